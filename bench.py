@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Benchmark of the EAT hot path (BASELINE.json metric: EAT queries/s and
+single-query ms; achieved bandwidth vs peak).
+
+Default workload (BASELINE.json configs[2], the batched city network): every
+rank solves a batch of 10,000 queries (1,000 random sources x 10 random
+departure times, the paper's protocol PAPER.md:458-460 scaled x10) on the
+synthetic ~10k-stop / ~30k-edge / ~2M-connection city timetable.  One step =
+one batch (every query runs the whole hot path: init, Cluster-AP relaxation
+sweeps to the fixpoint, output of e[] for all stops).  Queries are
+independent, so N ranks shard nothing: each rank gets its own 10k queries
+(weak scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Timing: CUDA events on the launching stream around each step's single
+kernel launch, L2 flushed (256 MiB write) between steps outside the events,
+barrier + synchronize around the K steps, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EAT queries/s"
+UNIT = "queries/s"
+QUERIES_PER_RANK = (1000, 10)  # sources x times
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _resolved(tt, ts):
+    """connections-effectively-resolved: sum over queries of |{c : dep_c >= t_s}|
+    (the set serial CSA must scan)."""
+    d = np.sort(tt.dep)
+    return int((d.size - np.searchsorted(d, ts, side="left")).sum())
+
+
+def _cpu_baseline(tt, src, ts, budget_s: float):
+    """Oracle (serial CSA, oracle/csa.c) as it stands, one host core, on a
+    bounded prefix of the same query list."""
+    import oracle
+
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    csa.query(int(src[0]), int(ts[0]))  # warm-up
+    t0 = time.perf_counter()
+    done = 0
+    while done < src.size and time.perf_counter() - t0 < budget_s:
+        k = min(64, src.size - done)
+        csa.query_many(src[done:done + k], ts[done:done + k])
+        done += k
+    dt = time.perf_counter() - t0
+    csa.close()
+    return {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {done} of the {src.size} city-batch queries, serial CSA (oracle/csa.c, gcc -O3), "
+                      f"{dt:.1f} s on 1 host core"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores (this tier's
+    reference arm), same workload/metric; rank 0 only."""
+    rank, world, _ = _dist()
+    if rank != 0:
+        return
+    import synth
+    import oracle
+
+    tt = synth.generate("city")
+    src, ts = synth.queries(tt, *QUERIES_PER_RANK)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    per_step = int(args.ref_queries)
+    for w in range(args.warmup):
+        csa.query_many(src[:8], ts[:8])
+    times = []
+    for k in range(args.steps):
+        sl = slice((k * per_step) % src.size, (k * per_step) % src.size + per_step)
+        t0 = time.perf_counter()
+        csa.query_many(src[sl], ts[sl])
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = per_step * args.steps / tot
+    sample = (f"{per_step} of the 10,000 city-batch queries per step, serial CSA (oracle/csa.c), 1 host core; "
+              f"steps time the bounded sample, queries/s extrapolates")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "city_batch_10k (BASELINE configs[2])", "stops": tt.num_vertices,
+                       "connections": tt.num_connections, "queries_per_step": per_step},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+
+    rank, world, local = _dist()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    import synth
+    from paper_1912_00966_b200 import Engine
+
+    tt = synth.generate("city")
+    nsrc, ntime = QUERIES_PER_RANK
+    all_src, all_ts = synth.queries(tt, nsrc * world, ntime)
+    per = nsrc * ntime
+    src, ts = all_src[rank * per:(rank + 1) * per], all_ts[rank * per:(rank + 1) * per]
+    nq = src.size
+    eng = Engine.from_timetable(tt, device=dev, kernel="auto")
+    st0 = eng.stats()
+    stream = torch.cuda.Stream(device=dev)
+    d_src = torch.tensor(src.astype(np.int32), device=dev)
+    d_ts = torch.tensor(ts.astype(np.int32), device=dev)
+    d_out = torch.empty((nq, tt.num_vertices), dtype=torch.int32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MiB > 126 MB L2
+
+    def step():
+        eng.query_many_device(d_src, d_ts, d_out, stream=stream)
+
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = Clocks(dev)
+    clocks.start()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k)
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * nq * args.steps / (tot_ms / 1e3)
+
+    # ---- e2e through the public API with host buffers (H2D queries, D2H all rows)
+    h_out = np.empty((nq, tt.num_vertices), dtype=np.uint32)
+    e2e_steps = max(1, min(args.steps, 3))
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        h_out = eng.query_many(src, ts)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * nq * e2e_steps / e2e_s
+
+    # ---- single-query latency (BASELINE configs[1]: s=0, t_s=06:00)
+    s1, t1 = synth.SINGLE_QUERY
+    o1 = torch.empty(tt.num_vertices, dtype=torch.int32, device=dev)
+    single = {}
+    for kname in ("cta", "frontier"):
+        e1 = Engine.from_timetable(tt, device=dev, kernel=kname)
+        for _ in range(3):
+            e1.query_device(s1, t1, o1, stream=stream)
+        stream.synchronize()
+        reps = 20
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            e1.query_device(s1, t1, o1, stream=stream)
+        b.record(stream)
+        b.synchronize()
+        single[kname] = {"ms": a.elapsed_time(b) / reps, "sweeps": e1.stats()["last_sweeps"]}
+        e1.close()
+
+    # ---- algorithmic bytes of the batched kernel (counters from an instrumented run)
+    roof = None
+    try:
+        from paper_1912_00966_b200 import counters
+
+        cnt = counters.count_batch(tt, src, ts, dev)
+        alg_bytes = cnt["algorithmic_bytes"]
+        mean_launch_s = (sum(step_ms) / len(step_ms)) / 1e3
+        peak, peak_src = _peaks()
+        achieved = alg_bytes / mean_launch_s / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic_city_batch.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src, "kernel": "k_query_cta",
+                "algorithmic_bytes_per_launch": alg_bytes, "counters": cnt}
+    except Exception as exc:  # keep the bench line even if accounting fails
+        roof = {"bound": "hbm", "achieved": None, "peak": _peaks()[0], "unit": "GB/s", "frac": None,
+                "traffic": None, "error": repr(exc)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = _cpu_baseline(tt, src, ts, args.cpu_seconds)
+
+    if rank == 0:
+        resolved = _resolved(tt, ts) * world * args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "city_batch_10k (BASELINE configs[2]; 10k queries per GPU)",
+                       "stops": tt.num_vertices, "edges": st0["num_edges"], "connections": tt.num_connections,
+                       "types": st0["num_types"], "queries_per_gpu": nq, "parallelism": f"query-sharded x{world}",
+                       "l2": "flushed (256 MiB write) between timed steps", "kernel": st0["kernel_name"],
+                       "subwarp": 8},
+            "connections_resolved_per_s": resolved / (tot_ms / 1e3),
+            "single_query_ms": {k: v["ms"] for k, v in single.items()},
+            "single_query_sweeps": {k: v["sweeps"] for k, v in single.items()},
+            "single_query_config": "city, s=0, t_s=06:00 (BASELINE configs[1]), device time per query",
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(nq * 8),
+                    "d2h_bytes_per_step": int(nq * tt.num_vertices * 4)},
+            "gpu_launches": args.steps,
+            "clocks": clk,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-queries", type=int, default=200)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,225 @@
+/*
+ * eat.h -- C ABI of libeat.so, the B200 earliest-arrival-time (EAT) engine.
+ *
+ * Method: arXiv 1912.00966, Haryan et al., "GPU Algorithm for Earliest
+ * Arrival Time Problem in Public Transport Networks".
+ *   - Problem: given connections (u, v, t, lambda), a
+ *     source s and a start time t_s, the earliest arrival time e[v] at every
+ *     vertex over time-respecting paths that leave s at or after t_s.
+ *   - Method: topology-driven relaxation sweeps.
+ *     Each sweep takes, for every connection type C_{u,v,lambda}
+ *     whose source u is active, the first departure >= e[u] through the
+ *     Cluster-AP hybrid rule (hour clusters + arithmetic progressions +
+ *     "first connection of the next non-empty cluster", PAPER.md:300-306,
+ *     Algorithm 6) and applies atomicMin to e[v]
+ *     (PAPER.md:403-409); double-buffered frontiers;
+ *     sweeps repeat until no vertex improves.
+ *
+ * Conventions (all entry points):
+ *   - Times are uint32 seconds; EAT_INF = 0x7FFFFFFF marks
+ *     "unreachable" (reading R2 in DESIGN.md).  Every finite time < EAT_INF.
+ *   - Vertex ids are the CALLER's ids 0..num_vertices-1 on input and output
+ *     (the engine renumbers internally for locality and maps back).
+ *   - Ownership: eat_build copies everything it needs; the caller may free its
+ *     arrays on return.  The handle owns all host and device memory it
+ *     allocates; outputs are caller-allocated.  eat_free(NULL) is a no-op.
+ *   - Errors: every call returns an eat_status; no C++ exception crosses the
+ *     ABI; on error outputs are left untouched (host variants) or unspecified
+ *     (device variants) and eat_last_error() returns a thread-local message.
+ *   - Threading: a handle is immutable after eat_build; calls on one handle
+ *     are serialised by an internal mutex; distinct handles are independent.
+ *   - There is no CPU fallback: every query runs in the CUDA kernels of
+ *     libeat.so; without a usable CUDA device the query calls return
+ *     EAT_ECUDA.
+ */
+#ifndef EAT_H
+#define EAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EAT_INF 0x7FFFFFFFu
+#define EAT_ABI_VERSION 1u
+
+typedef enum eat_status {
+    EAT_OK = 0,
+    EAT_EINVAL = 1,        /* bad argument: NULL pointer, id out of range, bad option */
+    EAT_ERANGE = 2,        /* a time >= EAT_INF (dep + dur, or t_s) */
+    EAT_ENOMEM = 3,        /* host or device allocation failed */
+    EAT_ECUDA = 4,         /* CUDA runtime error, or no CUDA device */
+    EAT_ENCCL = 5,         /* NCCL error (edge-partitioned mode) */
+    EAT_EUNSUPPORTED = 6,  /* option combination not supported by this build */
+    EAT_ESTATE = 7         /* call not valid for this handle (e.g. host-only handle) */
+} eat_status;
+
+/* Raw timetable, structure of arrays, one entry per connection
+ * (u, v, t=dep, lambda=dur).  Loops (u == v), lambda = 0
+ * and duplicate connections are accepted.  Arrays are read only during
+ * eat_build. */
+typedef struct eat_timetable {
+    uint32_t num_vertices;        /* |V| >= 1 */
+    uint64_t num_connections;     /* |C| >= 0 */
+    const uint32_t *u;            /* [num_connections] source vertex  (< num_vertices) */
+    const uint32_t *v;            /* [num_connections] target vertex  (< num_vertices) */
+    const uint32_t *dep;          /* [num_connections] departure t at u, seconds */
+    const uint32_t *dur;          /* [num_connections] duration lambda, seconds; dep+dur < EAT_INF */
+    const uint32_t *trip;         /* optional (NULL): trip id per connection (reserved) */
+    const float *xy;              /* optional (NULL): [2*num_vertices] stop coordinates */
+} eat_timetable;
+
+/* eat_build_opts.renumber: internal vertex order (a locality choice only;
+ * results are returned in caller ids either way). */
+enum {
+    EAT_RENUMBER_AUTO = 0,        /* MORTON if xy given, else BFS */
+    EAT_RENUMBER_NONE = 1,
+    EAT_RENUMBER_BFS = 2,
+    EAT_RENUMBER_MORTON = 3
+};
+
+/* eat_build_opts.kernel: relaxation schedule for single queries. */
+enum {
+    EAT_KERNEL_AUTO = 0,          /* CTA kernel when arr fits shared memory, else FRONTIER */
+    EAT_KERNEL_FRONTIER = 1,      /* grid-wide persistent kernel, worklist frontier, global arr */
+    EAT_KERNEL_FULL_SWEEP = 2,    /* grid-wide persistent kernel, every type every sweep, active bitmap */
+    EAT_KERNEL_CTA = 3            /* one CTA per query, arr in shared memory */
+};
+
+/* eat_build_opts.mode */
+enum {
+    EAT_MODE_REPLICATED = 0,      /* whole index on this device (query-parallel sharding is the caller's) */
+    EAT_MODE_EDGE_PARTITIONED = 1 /* this process owns the out-edges of a vertex range; NCCL min-allreduce */
+};
+
+/* eat_build_opts.flags */
+#define EAT_BUILD_HOST_ONLY 0x1u   /* compress only, no device upload: introspection (eat_index_*) */
+#define EAT_BUILD_COUNTERS 0x2u    /* batched kernel runs its instrumented variant (work counters in eat_stats) */
+
+typedef struct eat_build_opts {
+    uint32_t cluster_seconds;     /* hour-cluster width; 0 -> 3600; valid 1..4096 */
+    uint32_t renumber;            /* EAT_RENUMBER_* */
+    int32_t device;               /* CUDA device ordinal; -1 -> current device */
+    uint32_t kernel;              /* EAT_KERNEL_* */
+    uint32_t flags;               /* EAT_BUILD_* */
+    uint32_t subwarp;             /* lanes per vertex in the relax kernels: 0 -> 8; one of 1,2,4,8,16,32 */
+    uint32_t mode;                /* EAT_MODE_* */
+    uint32_t part_rank;           /* EDGE_PARTITIONED: this process's rank */
+    uint32_t part_count;          /* EDGE_PARTITIONED: number of ranks (1 = single partition) */
+    const void *nccl_unique_id;   /* EDGE_PARTITIONED with part_count > 1: 128-byte ncclUniqueId, same on every rank */
+} eat_build_opts;
+
+typedef struct eat_handle eat_handle;
+
+/* Build the compressed index (host) and upload it (device).  Steps:
+ * validate; renumber; CSR of connection types by source vertex (relation R,
+ * PAPER.md:225); per type, hour clusters covered by
+ * greedy arithmetic progressions packed as 32-byte cluster
+ * records; upload.  Untimed preprocessing, like the paper's.
+ * opts may be NULL (all defaults).  EDGE_PARTITIONED with part_count > 1 is
+ * collective: every rank must call it (it creates the NCCL communicator).
+ * Errors: EAT_EINVAL (NULL tt/out, num_vertices == 0, id >= num_vertices,
+ * bad option), EAT_ERANGE (dep + dur >= EAT_INF), EAT_ENOMEM, EAT_ECUDA,
+ * EAT_ENCCL. */
+eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_handle **out);
+
+/* One query (s, t_s) -> out_arr[num_vertices] (host memory), caller ids.
+ * out_arr[s] = t_s; unreachable vertices get EAT_INF (PAPER.md:58-59,
+ * Algorithm 2).  Copies the result device->host.
+ * Errors: EAT_EINVAL (s >= num_vertices, NULL out), EAT_ERANGE
+ * (t_s >= EAT_INF), EAT_ESTATE (host-only handle), EAT_ECUDA, EAT_ENCCL. */
+eat_status eat_query(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *out_arr);
+
+/* Same, device output: d_out is a device pointer [num_vertices] on the
+ * handle's device; work is enqueued on `cuda_stream` (a cudaStream_t, NULL =
+ * legacy default stream).  Returns after enqueue (the query's sweep count
+ * becomes available in eat_get_stats after the stream completes). */
+eat_status eat_query_device(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_out, void *cuda_stream);
+
+/* Batched independent queries (the paper's protocol):
+ * sources[i], times[i] for i < nq; out is row-major [nq][num_vertices] in
+ * host memory.  Each query is solved by one CTA of the batched kernel.
+ * Errors as eat_query (checked for every i before any work). */
+eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t *times, uint64_t nq,
+                          uint32_t *out);
+
+/* Same, all pointers device pointers on the handle's device, enqueued on
+ * cuda_stream.  Query validity (s < num_vertices, t_s < EAT_INF) is checked
+ * on the device: an invalid query yields a row of EAT_INF and sets the
+ * stats field `invalid_queries`. */
+eat_status eat_query_many_device(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
+                                 uint32_t *d_out, void *cuda_stream);
+
+/* Test/introspection entry point: the Cluster-AP lookup kernel alone
+ * (PAPER.md:305-306 with Algorithm 6).  For i < n: d_out[i] = the smallest
+ * departure >= d_bound[i] of internal connection type d_type[i], or EAT_INF.
+ * Device pointers, enqueued on cuda_stream.  EAT_EINVAL if any type id is
+ * out of range is NOT checked on the device: ids must be < num_types. */
+eat_status eat_lookup_device(eat_handle *h, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,
+                             uint32_t *d_out, void *cuda_stream);
+
+typedef struct eat_stats {
+    /* build */
+    uint32_t num_vertices;
+    uint32_t num_clusters;        /* max(24, ceil((max_dep+1)/cluster_seconds)) */
+    uint64_t num_connections;
+    uint64_t num_types;           /* connection types owned by this handle */
+    uint64_t num_edges;           /* distinct (u,v) owned by this handle */
+    uint64_t num_cluster_records; /* 32-byte cluster records */
+    uint64_t num_items;           /* AP items (runs + singletons) */
+    uint64_t num_spill_items;     /* items stored out of line */
+    uint64_t index_bytes;         /* device bytes of the packed index */
+    double build_ms;              /* host build wall time */
+    /* last single query (valid after its stream completed) */
+    uint32_t last_sweeps;         /* relaxation sweeps (incl. the final empty one) */
+    uint32_t last_rounds;         /* EDGE_PARTITIONED: exchange rounds */
+    uint64_t invalid_queries;     /* batched device variant: invalid (s, t_s) seen */
+    uint32_t kernel;              /* EAT_KERNEL_* actually used for single queries */
+    uint32_t smem_vertices_max;   /* largest |V| the CTA kernel keeps in shared memory */
+    /* EAT_BUILD_COUNTERS only: cumulative work of the batched kernel since build */
+    uint64_t vertex_visits;       /* active vertices processed (type_ptr pair read) */
+    uint64_t type_evals;          /* 32-byte type records read */
+    uint64_t cluster_reads;       /* 32-byte cluster records read (Cluster-AP lookups) */
+    uint64_t spill_items_read;    /* out-of-line AP items read */
+    uint64_t improvements;        /* successful atomicMin relaxations */
+    uint64_t sweeps_total;        /* relaxation sweeps summed over queries */
+} eat_stats;
+
+eat_status eat_get_stats(const eat_handle *h, eat_stats *out);
+
+/* Introspection of the packed index (host copy), for tests and tools.
+ * Layout: vertices are internal ids; perm[c] is
+ * the internal id of caller vertex c.  Types of internal vertex x are
+ * type_ptr[x] .. type_ptr[x+1]-1.  type_rec is [num_types][8] uint32:
+ * {v, lambda, first_dep, last_dep, crec_base, c_first, u, 0}.  crec is
+ * [num_cluster_records][8] uint32: {next_min, item0..item6} or a spill
+ * record {next_min, 0xFFFFFFFE, pool_offset, pool_count, ...}.  Items are
+ * uint32: bits 0-11 first offset in the cluster, 12-23 stride, 24-31
+ * count-1; 0xFFFFFFFF = empty slot.  Any pointer may be NULL to skip it.
+ * Sizes in elements are given by eat_index_sizes (type_ptr has
+ * num_vertices+1 entries). */
+eat_status eat_index_export(const eat_handle *h, uint32_t *perm, uint32_t *type_ptr, uint32_t *type_rec,
+                            uint32_t *crec, uint32_t *pool);
+
+/* Element counts of the (whole, unpartitioned) host index copy that
+ * eat_index_export writes: types, cluster records, spilled items.  Any
+ * pointer may be NULL.  Errors: EAT_EINVAL for a NULL handle. */
+eat_status eat_index_sizes(const eat_handle *h, uint64_t *num_types, uint64_t *num_cluster_records,
+                           uint64_t *num_pool_items);
+
+/* Internal-vertex range [*lo, *hi) whose out-types partition `rank` of
+ * `count` owns in EAT_MODE_EDGE_PARTITIONED (contiguous after renumbering,
+ * balanced by connection-type count).  Host-only; any handle.
+ * Errors: EAT_EINVAL (NULL handle/outputs, count == 0, rank >= count). */
+eat_status eat_partition_range(const eat_handle *h, uint32_t rank, uint32_t count, uint32_t *lo, uint32_t *hi);
+
+void eat_free(eat_handle *h);
+const char *eat_last_error(void);
+uint32_t eat_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EAT_H */

@@ -1,0 +1,533 @@
+// api.cu -- the C ABI of libeat.so (include/eat.h): handle lifecycle, device
+// upload (north-star subsystem 2: SoA arrays packed for 128-bit loads),
+// query drivers for the kernels in kernels.cu, and the edge-partitioned
+// multi-GPU driver (NCCL min-allreduce of e[] per exchange round).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "eat.h"
+#include "eat_internal.h"
+#include "kernels.cuh"
+#include "partition.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+eat_status fail(eat_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                           \
+    do {                                                                                         \
+        cudaError_t _e = (expr);                                                                 \
+        if (_e != cudaSuccess)                                                                   \
+            return fail(EAT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));          \
+    } while (0)
+
+#define NCCL_TRY(expr)                                                                           \
+    do {                                                                                         \
+        ncclResult_t _r = (expr);                                                                \
+        if (_r != ncclSuccess) return fail(EAT_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+template <class T>
+cudaError_t dalloc_copy(T **dst, const T *src, size_t count, size_t &bytes) {
+    *dst = nullptr;
+    size_t b = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(dst, b);
+    if (e != cudaSuccess) return e;
+    bytes += b;
+    if (count) e = cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+}  // namespace
+
+struct eat_handle {
+    std::mutex mu;
+    eat::HostIndex hx;
+    bool host_only = false;
+    int device = 0;
+    uint32_t kernel = EAT_KERNEL_AUTO;   // resolved single-query kernel
+    uint32_t subwarp = 8;
+    uint32_t mode = EAT_MODE_REPLICATED;
+    cudaStream_t stream = nullptr;
+    // device index
+    uint32_t *d_type_ptr = nullptr, *d_type_rec = nullptr, *d_crec = nullptr, *d_pool = nullptr;
+    uint32_t *d_type_src = nullptr, *d_perm = nullptr;
+    eat::DevIndex ix{};
+    size_t index_bytes = 0;
+    // single-query scratch
+    eat::GridWork gw{};
+    uint32_t *d_out1 = nullptr, *h_out1 = nullptr;
+    uint32_t *d_q1 = nullptr;  // [2]: s, t_s for the CTA kernel
+    uint32_t *d_sweeps1 = nullptr;
+    unsigned long long *d_counter = nullptr, *d_invalid = nullptr;
+    unsigned long long *d_work = nullptr;  // EAT_BUILD_COUNTERS: 6 work counters
+    // batched scratch
+    uint32_t *d_bsrc = nullptr, *d_bts = nullptr, *d_bout = nullptr;
+    uint64_t bcap = 0;
+    int cta_grid = 0;
+    // edge partition
+    uint32_t part_rank = 0, part_count = 1, part_lo = 0, part_hi = 0;
+    ncclComm_t comm = nullptr;
+    eat::PartWork pw{};
+    // stats
+    eat_stats st{};
+};
+
+namespace {
+
+void release_device(eat_handle *h) {
+    if (h->host_only) return;
+    cudaSetDevice(h->device);
+    void *ptrs[] = {h->d_type_ptr, h->d_type_rec, h->d_crec, h->d_pool, h->d_type_src, h->d_perm,
+                    h->gw.arr,     h->gw.q0,      h->gw.q1,  h->gw.stamp, h->gw.bm,  h->gw.ctl,
+                    h->d_out1,     h->d_q1,       h->d_sweeps1, h->d_counter, h->d_invalid, h->d_bsrc,
+                    h->d_bts,      h->d_bout,     h->d_work};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    eat::part_free(h->pw);
+    if (h->h_out1) cudaFreeHost(h->h_out1);
+    if (h->comm) ncclCommDestroy(h->comm);
+    if (h->stream) cudaStreamDestroy(h->stream);
+}
+
+eat_status upload(eat_handle *h) {
+    const eat::HostIndex &x = h->hx;
+    const uint32_t n = x.n;
+    // Slice of the index owned by this partition: sources [lo, hi).
+    uint32_t lo = 0, hi = n;
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED) eat::partition_range(x, h->part_rank, h->part_count, lo, hi);
+    h->part_lo = lo;
+    h->part_hi = hi;
+    const uint32_t t_lo = x.type_ptr[lo], t_hi = x.type_ptr[hi];
+    const uint64_t T = t_hi - t_lo;
+    uint64_t r_lo = 0, r_hi = 0, p_lo = 0, p_hi = 0;
+    if (T) {
+        r_lo = x.type_rec[uint64_t(t_lo) * eat::kTypeWords + 4];
+        r_hi = (t_hi < x.num_types) ? x.type_rec[uint64_t(t_hi) * eat::kTypeWords + 4] : x.num_crec;
+        // pool range: spilled records in [r_lo, r_hi) are contiguous in pool order
+        p_lo = x.pool.size();
+        p_hi = 0;
+        for (uint64_t r = r_lo; r < r_hi; ++r)
+            if (x.crec[r * eat::kCrecWords + 1] == eat::kItemSpill) {
+                p_lo = std::min<uint64_t>(p_lo, x.crec[r * eat::kCrecWords + 2]);
+                p_hi = std::max<uint64_t>(p_hi, uint64_t(x.crec[r * eat::kCrecWords + 2]) + x.crec[r * eat::kCrecWords + 3]);
+            }
+        if (p_hi < p_lo) p_lo = p_hi = 0;
+    }
+    std::vector<uint32_t> tptr(uint64_t(n) + 1);
+    for (uint64_t i = 0; i <= n; ++i) {
+        uint32_t c = std::min(std::max(x.type_ptr[i], t_lo), t_hi);
+        tptr[i] = c - t_lo;
+    }
+    std::vector<uint32_t> trec(x.type_rec.begin() + uint64_t(t_lo) * eat::kTypeWords,
+                               x.type_rec.begin() + uint64_t(t_hi) * eat::kTypeWords);
+    std::vector<uint32_t> tsrc(T);
+    for (uint64_t t = 0; t < T; ++t) {
+        trec[t * eat::kTypeWords + 4] -= uint32_t(r_lo);
+        tsrc[t] = trec[t * eat::kTypeWords + 6];
+    }
+    std::vector<uint32_t> crec(x.crec.begin() + r_lo * eat::kCrecWords, x.crec.begin() + r_hi * eat::kCrecWords);
+    for (uint64_t r = 0; r < r_hi - r_lo; ++r)
+        if (crec[r * eat::kCrecWords + 1] == eat::kItemSpill) crec[r * eat::kCrecWords + 2] -= uint32_t(p_lo);
+    size_t &b = h->index_bytes;
+    CUDA_TRY(dalloc_copy(&h->d_type_ptr, tptr.data(), tptr.size(), b));
+    CUDA_TRY(dalloc_copy(&h->d_type_rec, trec.data(), trec.size(), b));
+    CUDA_TRY(dalloc_copy(&h->d_crec, crec.data(), crec.size(), b));
+    CUDA_TRY(dalloc_copy(&h->d_pool, x.pool.data() + p_lo, p_hi - p_lo, b));
+    CUDA_TRY(dalloc_copy(&h->d_type_src, tsrc.data(), tsrc.size(), b));
+    CUDA_TRY(dalloc_copy(&h->d_perm, x.perm.data(), x.perm.size(), b));
+    h->ix.n = n;
+    h->ix.cs = x.cs;
+    h->ix.num_types = T;
+    h->ix.type_ptr = h->d_type_ptr;
+    h->ix.type_rec = reinterpret_cast<const uint4 *>(h->d_type_rec);
+    h->ix.crec = reinterpret_cast<const uint4 *>(h->d_crec);
+    h->ix.pool = h->d_pool;
+    h->ix.type_src = h->d_type_src;
+    h->ix.perm = h->d_perm;
+    h->st.num_types = T;
+    h->st.num_cluster_records = r_hi - r_lo;
+    h->st.num_spill_items = p_hi - p_lo;
+    h->st.index_bytes = h->index_bytes;
+    // scratch
+    const uint64_t W = (n + 31ull) / 32ull;
+    CUDA_TRY(cudaMalloc(&h->gw.arr, n * 4ull));
+    CUDA_TRY(cudaMalloc(&h->gw.q0, n * 4ull));
+    CUDA_TRY(cudaMalloc(&h->gw.q1, n * 4ull));
+    CUDA_TRY(cudaMalloc(&h->gw.stamp, n * 4ull));
+    CUDA_TRY(cudaMalloc(&h->gw.bm, 3 * W * 4ull));
+    CUDA_TRY(cudaMalloc(&h->gw.ctl, 16 * 4));
+    CUDA_TRY(cudaMemset(h->gw.ctl, 0, 16 * 4));
+    CUDA_TRY(cudaMalloc(&h->d_out1, n * 4ull));
+    CUDA_TRY(cudaMallocHost(&h->h_out1, n * 4ull + 64));
+    CUDA_TRY(cudaMalloc(&h->d_q1, 2 * 4));
+    CUDA_TRY(cudaMalloc(&h->d_sweeps1, 4));
+    CUDA_TRY(cudaMalloc(&h->d_counter, 8));
+    CUDA_TRY(cudaMalloc(&h->d_invalid, 8));
+    CUDA_TRY(cudaMemset(h->d_invalid, 0, 8));
+    return EAT_OK;
+}
+
+eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
+    h->cta_grid = eat::cta_grid_size(h->hx.n, int(h->subwarp));
+    h->st.smem_vertices_max = 0;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    h->st.smem_vertices_max = uint32_t((size_t(optin) - 64) * 32 / (4 * 32 + 2 * 4));
+    uint32_t k = requested;
+    if (k == EAT_KERNEL_AUTO) k = h->cta_grid > 0 ? EAT_KERNEL_CTA : EAT_KERNEL_FRONTIER;
+    if (k == EAT_KERNEL_CTA && h->cta_grid == 0)
+        return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
+    if (k > EAT_KERNEL_CTA) return fail(EAT_EINVAL, "unknown kernel");
+    h->kernel = k;
+    h->st.kernel = k;
+    return EAT_OK;
+}
+
+eat_status check_query(const eat_handle *h, uint32_t s, uint32_t t_s) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
+    if (s >= h->hx.n) return fail(EAT_EINVAL, "invalid source vertex id");
+    if (t_s >= EAT_INF) return fail(EAT_ERANGE, "t_s >= EAT_INF");
+    return EAT_OK;
+}
+
+// Enqueue one single query on stream st writing caller-ordered e[] to d_out.
+eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_out, cudaStream_t st) {
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
+        return fail(EAT_ESTATE, "edge-partitioned handles run through eat_query / eat_query_device (internal)");
+    if (h->kernel == EAT_KERNEL_CTA) {
+        uint32_t q[2] = {s, t_s};
+        CUDA_TRY(cudaMemcpyAsync(h->d_q1, q, sizeof(q), cudaMemcpyHostToDevice, st));
+        CUDA_TRY(eat::launch_query_cta(h->ix, int(h->subwarp), h->d_q1, h->d_q1 + 1, 1, d_out, h->d_sweeps1,
+                                       h->d_counter, h->d_invalid, 1, nullptr, st));
+    } else {
+        int sched = h->kernel == EAT_KERNEL_FULL_SWEEP ? eat::kSchedFull : eat::kSchedFrontier;
+        CUDA_TRY(eat::launch_query_grid(h->ix, int(h->subwarp), sched, h->gw, s, t_s, d_out, st));
+        CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->gw.ctl + 8, 4, cudaMemcpyDeviceToDevice, st));
+    }
+    return EAT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t eat_abi_version(void) { return EAT_ABI_VERSION; }
+
+const char *eat_last_error(void) { return g_err.c_str(); }
+
+eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_handle **out) {
+    if (!tt || !out) return fail(EAT_EINVAL, "NULL timetable or output handle pointer");
+    eat_build_opts o{};
+    if (opts) o = *opts;
+    eat::BuildParams p;
+    p.cs = o.cluster_seconds ? o.cluster_seconds : 3600;
+    p.renumber = o.renumber;
+    const uint32_t sw = o.subwarp ? o.subwarp : 8;
+    if (sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
+        return fail(EAT_EINVAL, "subwarp must be 1, 2, 4, 8, 16 or 32");
+    if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
+    if (o.kernel > EAT_KERNEL_CTA) return fail(EAT_EINVAL, "unknown kernel");
+    uint32_t pc = o.part_count ? o.part_count : 1;
+    if (o.mode == EAT_MODE_EDGE_PARTITIONED && (o.part_rank >= pc || (pc > 1 && !o.nccl_unique_id)))
+        return fail(EAT_EINVAL, "edge partition needs part_rank < part_count and an NCCL unique id");
+    eat_handle *h = new (std::nothrow) eat_handle();
+    if (!h) return fail(EAT_ENOMEM, "out of host memory");
+    h->subwarp = sw;
+    h->mode = o.mode;
+    h->part_rank = o.part_rank;
+    h->part_count = pc;
+    h->host_only = (o.flags & EAT_BUILD_HOST_ONLY) != 0;
+    std::string msg;
+    int rc;
+    try {
+        rc = eat::build_host_index(tt->num_vertices, tt->num_connections, tt->u, tt->v, tt->dep, tt->dur, tt->xy,
+                                   p, h->hx, msg);
+    } catch (const std::bad_alloc &) {
+        rc = EAT_ENOMEM;
+        msg = "out of host memory during build";
+    }
+    if (rc != EAT_OK) {
+        delete h;
+        return fail(eat_status(rc), msg);
+    }
+    eat_stats &s = h->st;
+    s.num_vertices = h->hx.n;
+    s.num_clusters = h->hx.num_clusters;
+    s.num_connections = h->hx.m;
+    s.num_types = h->hx.num_types;
+    s.num_edges = h->hx.num_edges;
+    s.num_cluster_records = h->hx.num_crec;
+    s.num_items = h->hx.num_items;
+    s.num_spill_items = h->hx.pool.size();
+    s.build_ms = h->hx.build_ms;
+    if (h->host_only) {
+        *out = h;
+        return EAT_OK;
+    }
+    eat_status est = EAT_OK;
+    do {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            est = fail(EAT_ECUDA, "no CUDA device available (libeat has no CPU fallback)");
+            break;
+        }
+        if (o.device >= 0) {
+            if (o.device >= ndev) {
+                est = fail(EAT_EINVAL, "device ordinal out of range");
+                break;
+            }
+            h->device = o.device;
+        } else {
+            cudaGetDevice(&h->device);
+        }
+        if (cudaSetDevice(h->device) != cudaSuccess || cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            est = fail(EAT_ECUDA, "cannot initialise CUDA device");
+            break;
+        }
+        est = upload(h);
+        if (est != EAT_OK) break;
+        est = resolve_kernel(h, o.kernel);
+        if (est != EAT_OK) break;
+        if (o.flags & EAT_BUILD_COUNTERS) {
+            if (cudaMalloc(&h->d_work, 6 * sizeof(unsigned long long)) != cudaSuccess ||
+                cudaMemset(h->d_work, 0, 6 * sizeof(unsigned long long)) != cudaSuccess) {
+                est = fail(EAT_ENOMEM, "cannot allocate work counters");
+                break;
+            }
+        }
+        if (h->mode == EAT_MODE_EDGE_PARTITIONED) {
+            if (pc > 1) {
+                ncclUniqueId id;
+                std::memcpy(&id, o.nccl_unique_id, sizeof(id));
+                ncclResult_t r = ncclCommInitRank(&h->comm, int(pc), id, int(o.part_rank));
+                if (r != ncclSuccess) {
+                    est = fail(EAT_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+                    break;
+                }
+            }
+            if (eat::part_alloc(h->pw, h->hx.n) != cudaSuccess) {
+                est = fail(EAT_ENOMEM, "cannot allocate partition scratch");
+                break;
+            }
+        }
+    } while (0);
+    if (est != EAT_OK) {
+        std::string keep = g_err;
+        release_device(h);
+        delete h;
+        g_err = keep;
+        return est;
+    }
+    *out = h;
+    return EAT_OK;
+}
+
+void eat_free(eat_handle *h) {
+    if (!h) return;
+    release_device(h);
+    delete h;
+}
+
+eat_status eat_get_stats(const eat_handle *hc, eat_stats *out) {
+    if (!hc || !out) return fail(EAT_EINVAL, "NULL argument");
+    eat_handle *h = const_cast<eat_handle *>(hc);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->host_only) {
+        cudaSetDevice(h->device);
+        uint32_t sw = 0;
+        unsigned long long inv = 0;
+        CUDA_TRY(cudaMemcpy(&sw, h->d_sweeps1, 4, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(&inv, h->d_invalid, 8, cudaMemcpyDeviceToHost));
+        h->st.last_sweeps = sw;
+        h->st.invalid_queries = inv;
+        if (h->d_work) {
+            unsigned long long w[6];
+            CUDA_TRY(cudaMemcpy(w, h->d_work, sizeof(w), cudaMemcpyDeviceToHost));
+            h->st.vertex_visits = w[0];
+            h->st.type_evals = w[1];
+            h->st.cluster_reads = w[2];
+            h->st.spill_items_read = w[3];
+            h->st.improvements = w[4];
+            h->st.sweeps_total = w[5];
+        }
+    }
+    *out = h->st;
+    return EAT_OK;
+}
+
+eat_status eat_query_device(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_out, void *cuda_stream) {
+    eat_status e = check_query(h, s, t_s);
+    if (e != EAT_OK) return e;
+    if (!d_out) return fail(EAT_EINVAL, "NULL output");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_TRY(cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED) {
+        uint32_t rounds = 0, sweeps = 0;
+        e = eat::part_query(h->ix, h->pw, h->comm, h->part_lo, h->part_hi, int(h->subwarp), s, t_s, d_out, st,
+                            &rounds, &sweeps, g_err);
+        h->st.last_rounds = rounds;
+        CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, &h->pw.h_sweeps, 4, cudaMemcpyHostToDevice, st));
+        return e;
+    }
+    return enqueue_single(h, s, t_s, d_out, st);
+}
+
+eat_status eat_query(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *out_arr) {
+    eat_status e = check_query(h, s, t_s);
+    if (e != EAT_OK) return e;
+    if (!out_arr) return fail(EAT_EINVAL, "NULL output");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_TRY(cudaSetDevice(h->device));
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED) {
+        uint32_t rounds = 0, sweeps = 0;
+        e = eat::part_query(h->ix, h->pw, h->comm, h->part_lo, h->part_hi, int(h->subwarp), s, t_s, h->d_out1,
+                            h->stream, &rounds, &sweeps, g_err);
+        if (e != EAT_OK) return e;
+        h->st.last_rounds = rounds;
+        CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, &h->pw.h_sweeps, 4, cudaMemcpyHostToDevice, h->stream));
+    } else {
+        e = enqueue_single(h, s, t_s, h->d_out1, h->stream);
+        if (e != EAT_OK) return e;
+    }
+    CUDA_TRY(cudaMemcpyAsync(h->h_out1, h->d_out1, h->hx.n * 4ull, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    std::memcpy(out_arr, h->h_out1, h->hx.n * 4ull);
+    return EAT_OK;
+}
+
+eat_status eat_query_many_device(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
+                                 uint32_t *d_out, void *cuda_stream) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
+    if (nq == 0) return EAT_OK;
+    if (!d_sources || !d_times || !d_out) return fail(EAT_EINVAL, "NULL argument");
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
+        return fail(EAT_ESTATE, "batched queries need a replicated handle (query-parallel sharding)");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_TRY(cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (h->cta_grid > 0) {
+        CUDA_TRY(eat::launch_query_cta(h->ix, int(h->subwarp), d_sources, d_times, nq, d_out, nullptr, h->d_counter,
+                                       h->d_invalid, 0, h->d_work, st));
+        return EAT_OK;
+    }
+    // |V| too large for shared memory: one grid-wide query after another
+    std::vector<uint32_t> hs(nq), ht(nq);
+    CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sources, nq * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(ht.data(), d_times, nq * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (uint64_t q = 0; q < nq; ++q) {
+        uint32_t *row = d_out + q * uint64_t(h->hx.n);
+        if (hs[q] >= h->hx.n || ht[q] >= EAT_INF) {
+            CUDA_TRY(cudaMemsetAsync(row, 0xFF, h->hx.n * 4ull, st));  // 0xFFFFFFFF then fixed below
+            std::vector<uint32_t> inf(h->hx.n, EAT_INF);
+            CUDA_TRY(cudaMemcpyAsync(row, inf.data(), h->hx.n * 4ull, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            continue;
+        }
+        int sched = h->kernel == EAT_KERNEL_FULL_SWEEP ? eat::kSchedFull : eat::kSchedFrontier;
+        CUDA_TRY(eat::launch_query_grid(h->ix, int(h->subwarp), sched, h->gw, hs[q], ht[q], row, st));
+    }
+    return EAT_OK;
+}
+
+eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t *times, uint64_t nq,
+                          uint32_t *out) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
+    if (nq == 0) return EAT_OK;
+    if (!sources || !times || !out) return fail(EAT_EINVAL, "NULL argument");
+    for (uint64_t q = 0; q < nq; ++q) {
+        if (sources[q] >= h->hx.n) return fail(EAT_EINVAL, "invalid source vertex id at index " + std::to_string(q));
+        if (times[q] >= EAT_INF) return fail(EAT_ERANGE, "t_s >= EAT_INF at index " + std::to_string(q));
+    }
+    const uint64_t n = h->hx.n;
+    // chunk so that the device output buffer stays <= 1 GiB
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(nq, (1ull << 30) / (4 * n)));
+    {
+        std::lock_guard<std::mutex> lk(h->mu);
+        CUDA_TRY(cudaSetDevice(h->device));
+        if (h->bcap < chunk) {
+            if (h->d_bsrc) cudaFree(h->d_bsrc);
+            if (h->d_bts) cudaFree(h->d_bts);
+            if (h->d_bout) cudaFree(h->d_bout);
+            h->d_bsrc = h->d_bts = h->d_bout = nullptr;
+            h->bcap = 0;
+            CUDA_TRY(cudaMalloc(&h->d_bsrc, chunk * 4));
+            CUDA_TRY(cudaMalloc(&h->d_bts, chunk * 4));
+            CUDA_TRY(cudaMalloc(&h->d_bout, chunk * n * 4));
+            h->bcap = chunk;
+        }
+    }
+    for (uint64_t q0 = 0; q0 < nq; q0 += chunk) {
+        const uint64_t c = std::min(chunk, nq - q0);
+        {
+            std::lock_guard<std::mutex> lk(h->mu);
+            CUDA_TRY(cudaMemcpyAsync(h->d_bsrc, sources + q0, c * 4, cudaMemcpyHostToDevice, h->stream));
+            CUDA_TRY(cudaMemcpyAsync(h->d_bts, times + q0, c * 4, cudaMemcpyHostToDevice, h->stream));
+        }
+        eat_status e = eat_query_many_device(h, h->d_bsrc, h->d_bts, c, h->d_bout, h->stream);
+        if (e != EAT_OK) return e;
+        std::lock_guard<std::mutex> lk(h->mu);
+        CUDA_TRY(cudaMemcpyAsync(out + q0 * n, h->d_bout, c * n * 4, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
+    return EAT_OK;
+}
+
+eat_status eat_lookup_device(eat_handle *h, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,
+                             uint32_t *d_out, void *cuda_stream) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
+    if (n && (!d_type || !d_bound || !d_out)) return fail(EAT_EINVAL, "NULL argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_TRY(cudaSetDevice(h->device));
+    CUDA_TRY(eat::launch_lookup(h->ix, d_type, d_bound, n, d_out, static_cast<cudaStream_t>(cuda_stream)));
+    return EAT_OK;
+}
+
+eat_status eat_index_export(const eat_handle *h, uint32_t *perm, uint32_t *type_ptr, uint32_t *type_rec,
+                            uint32_t *crec, uint32_t *pool) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    const eat::HostIndex &x = h->hx;
+    if (perm) std::copy(x.perm.begin(), x.perm.end(), perm);
+    if (type_ptr) std::copy(x.type_ptr.begin(), x.type_ptr.end(), type_ptr);
+    if (type_rec) std::copy(x.type_rec.begin(), x.type_rec.end(), type_rec);
+    if (crec) std::copy(x.crec.begin(), x.crec.end(), crec);
+    if (pool) std::copy(x.pool.begin(), x.pool.end(), pool);
+    return EAT_OK;
+}
+
+eat_status eat_partition_range(const eat_handle *h, uint32_t rank, uint32_t count, uint32_t *lo, uint32_t *hi) {
+    if (!h || !lo || !hi || count == 0 || rank >= count) return fail(EAT_EINVAL, "bad partition arguments");
+    eat::partition_range(h->hx, rank, count, *lo, *hi);
+    return EAT_OK;
+}
+
+eat_status eat_index_sizes(const eat_handle *h, uint64_t *num_types, uint64_t *num_cluster_records,
+                           uint64_t *num_pool_items) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    if (num_types) *num_types = h->hx.num_types;
+    if (num_cluster_records) *num_cluster_records = h->hx.num_crec;
+    if (num_pool_items) *num_pool_items = h->hx.pool.size();
+    return EAT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// device_common.cuh -- device helpers shared by kernels.cu and partition.cu:
+// the Cluster-AP lookup (Algorithm 6),
+// the type-record load, a grid-wide barrier and warp-aggregated worklist push.
+#pragma once
+#include <cuda/atomic>
+#include <cuda_runtime.h>
+
+#include "eat_internal.h"
+#include "kernels.cuh"
+
+namespace eat {
+namespace dev {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
+
+// First term >= x of one packed AP item, as an offset inside the cluster;
+// kNone if the item is empty or all its terms are < x.  Algorithm 6 lines 3-8
+// (PAPER.md:288-294): x <= start -> start; start < x <= end ->
+// start + ceil((x - start) / difference) * difference.
+__device__ __forceinline__ uint32_t item_next(uint32_t it, uint32_t x) {
+    if (it == kItemEmpty) return kNone;
+    const uint32_t off = it & 0xFFFu, stride = (it >> 12) & 0xFFFu, cm1 = it >> 24;
+    if (x <= off) return off;
+    const uint32_t last = off + cm1 * stride;
+    if (x > last) return kNone;  // also covers singletons (cm1 == 0): stride unused
+    const uint32_t q = (x - off + stride - 1u) / stride;
+    return off + q * stride;
+}
+
+// Cluster-AP lookup inside the type's cluster k = eu / cs:
+// smallest term >= eu among the cluster's APs, else the first departure of
+// the next non-empty cluster (precomputed as next_min).
+// Precondition: first < eu <= last (so c_first <= k <= c_last).
+__device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t crec_base, uint32_t c_first,
+                                                   uint32_t eu) {
+    const uint32_t k = eu / ix.cs;
+    const uint32_t r = crec_base + (k - c_first);
+    const uint4 r0 = __ldg(ix.crec + 2ull * r);
+    const uint32_t x = eu - k * ix.cs;
+    uint32_t best;
+    if (r0.y == kItemSpill) {
+        best = kNone;
+        for (uint32_t i = 0; i < r0.w; ++i) best = min(best, item_next(__ldg(ix.pool + r0.z + i), x));
+    } else {
+        const uint4 r1 = __ldg(ix.crec + 2ull * r + 1);
+        best = min(min(item_next(r0.y, x), item_next(r0.z, x)), min(item_next(r0.w, x), item_next(r1.x, x)));
+        best = min(best, min(min(item_next(r1.y, x), item_next(r1.z, x)), item_next(r1.w, x)));
+    }
+    return best != kNone ? k * ix.cs + best : r0.x;
+}
+
+struct TypeRec {
+    uint32_t v, lam, first, last, crec_base, c_first;
+};
+
+__device__ __forceinline__ TypeRec load_type(const DevIndex &ix, uint64_t t) {
+    const uint4 a = __ldg(ix.type_rec + 2 * t);
+    const uint4 b = __ldg(ix.type_rec + 2 * t + 1);
+    return TypeRec{a.x, a.y, a.z, a.w, b.x, b.y};
+}
+
+// getConnection for one type (PAPER.md:226 semantics): first departure >= eu, or kInf.
+__device__ __forceinline__ uint32_t type_next_departure(const DevIndex &ix, const TypeRec &tr, uint32_t eu) {
+    if (eu > tr.last) return kInf;
+    if (eu <= tr.first) return tr.first;
+    return cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+}
+
+// ---------------------------------------------------------------- grid barrier
+__device__ __forceinline__ void grid_sync(uint32_t *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cnt(bar[0]);
+        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> gen(bar[1]);
+        const uint32_t g = gen.load(cuda::memory_order_relaxed);
+        __threadfence();
+        if (cnt.fetch_add(1u, cuda::memory_order_acq_rel) == gridDim.x - 1u) {
+            cnt.store(0u, cuda::memory_order_relaxed);
+            gen.fetch_add(1u, cuda::memory_order_release);
+        } else {
+            while (gen.load(cuda::memory_order_acquire) == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Warp-aggregated append of v to a worklist (one global atomic per group of
+// converged pushing lanes).
+__device__ __forceinline__ void push_aggregated(uint32_t v, uint32_t *q, uint32_t *count) {
+    const unsigned am = __activemask();
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned leader = __ffs(am) - 1u;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(count, uint32_t(__popc(am)));
+    base = __shfl_sync(am, base, leader);
+    q[base + __popc(am & ((1u << lane) - 1u))] = v;
+}
+
+// Relax one connection type (Algorithm 3) whose source has
+// arrival eu, against a global e[] (atomicMin).  Returns
+// the target v when this call strictly lowered e[v], else kNone.
+__device__ __forceinline__ uint32_t relax_type_global(const DevIndex &ix, uint64_t t, uint32_t eu, uint32_t *arr) {
+    const TypeRec tr = load_type(ix, t);
+    if (eu > tr.last) return kNone;
+    const uint32_t av = __ldcg(arr + tr.v);
+    if (max(eu, tr.first) + tr.lam >= av) return kNone;  // early termination
+    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+    const uint32_t cand = tc + tr.lam;
+    if (cand >= av) return kNone;
+    const uint32_t old = atomicMin(arr + tr.v, cand);
+    return cand < old ? tr.v : kNone;
+}
+
+}  // namespace dev
+}  // namespace eat

@@ -1,0 +1,371 @@
+// kernels.cu -- sm_100a relaxation kernels of the EAT hot path (north-star
+// subsystem 3).  Integer, irregular, latency/memory bound: no tensor cores.
+//
+// Per sweep, every active source u (frontier) reads
+// e[u] once; the lanes of its sub-warp (virtual warp) take
+// u's connection types (contiguous per edge)
+// and for each:
+//   - early termination: skip if e[u] > last departure or
+//     max(e[u], first) + lambda >= e[v];
+//   - Cluster-AP lookup (PAPER.md:300-306 + Algorithm 6):
+//     first departure >= e[u] via one 32-byte cluster record;
+//   - Relax (Algorithm 3) as atomicMin on e[v]
+//     (PAPER.md:403-409); a strict improvement marks v in the NEXT frontier.
+// Sweeps repeat until the next frontier is empty.
+#include <algorithm>
+#include <cuda/atomic>
+#include <cuda_runtime.h>
+
+#include "device_common.cuh"
+#include "eat_internal.h"
+#include "kernels.cuh"
+
+namespace eat {
+
+namespace {
+
+using namespace dev;
+
+// ---------------------------------------------------------------- lookup kernel
+__global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *bound, uint64_t n, uint32_t *out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const TypeRec tr = load_type(ix, type[i]);
+        out[i] = type_next_departure(ix, tr, bound[i]);
+    }
+}
+
+// ---------------------------------------------------------------- CTA kernel
+// One CTA solves one query at a time with e[] in shared memory (40 KB for a
+// 10k-stop city): sweeps are separated by __syncthreads instead of grid-wide
+// barriers, and relaxation is chaotic inside a sweep (updates are visible at
+// once; a vertex lowered after it was read is re-marked).
+// Queries are taken dynamically from a global counter (persistent grid).
+constexpr int kCtaThreads = 512;
+
+// COUNT: instrumented variant (EAT_BUILD_COUNTERS) accumulating, per launch,
+// the work counters used for algorithmic-byte accounting:
+// counters[0] vertex visits, [1] type records read, [2] cluster records read,
+// [3] spilled items read, [4] improvements (successful atomicMin), [5] sweeps.
+template <int SW, bool COUNT>
+__global__ void __launch_bounds__(kCtaThreads) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
+                                                            const uint32_t *__restrict__ tsv, uint64_t nq,
+                                                            uint32_t *__restrict__ out, uint32_t *sweeps_out,
+                                                            unsigned long long *qcounter,
+                                                            unsigned long long *invalid,
+                                                            unsigned long long *counters) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t n = ix.n;
+    const uint32_t W = (n + 31u) / 32u;
+    const uint32_t npad = (n + 3u) & ~3u;
+    uint32_t *arr = sm;
+    volatile uint32_t *varr = sm;
+    uint32_t *bmA = sm + npad;
+    uint32_t *bmB = bmA + W;
+    __shared__ unsigned long long s_q;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t lane = tid % SW, sub = tid / SW, nsub = kCtaThreads / SW;
+
+    for (;;) {
+        if (tid == 0) s_q = atomicAdd(qcounter, 1ull);
+        __syncthreads();
+        const unsigned long long q = s_q;
+        if (q >= nq) break;
+        const uint32_t s = src[q], ts = tsv[q];
+        uint32_t *orow = out + q * uint64_t(n);
+        if (s >= n || ts >= kInf) {
+            for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = kInf;
+            if (tid == 0) {
+                atomicAdd(invalid, 1ull);
+                if (sweeps_out) sweeps_out[q] = 0;
+            }
+            __syncthreads();
+            continue;
+        }
+        // Initialize (Algorithm 2)
+        for (uint32_t i = tid; i < n; i += kCtaThreads) arr[i] = kInf;
+        for (uint32_t i = tid; i < W; i += kCtaThreads) {
+            bmA[i] = 0;
+            bmB[i] = 0;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
+            arr[si] = ts;
+            bmA[si >> 5] = 1u << (si & 31u);
+        }
+        __syncthreads();
+        uint32_t *cur = bmA, *nxt = bmB;
+        uint32_t sweeps = 0;
+        uint32_t c_vis = 0, c_type = 0, c_crec = 0, c_spill = 0, c_impr = 0;
+        for (;;) {
+            for (uint32_t wi = sub; wi < W; wi += nsub) {
+                uint32_t word = cur[wi];
+                while (word) {
+                    const uint32_t b = __ffs(word) - 1u;
+                    word &= word - 1u;
+                    const uint32_t x = wi * 32u + b;
+                    const uint32_t eu = varr[x];
+                    const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
+                    if (COUNT && lane == 0) ++c_vis;
+                    for (uint32_t t = p0 + lane; t < p1; t += SW) {
+                        const TypeRec tr = load_type(ix, t);
+                        if (COUNT) ++c_type;
+                        if (eu > tr.last) continue;
+                        const uint32_t av = varr[tr.v];
+                        if (max(eu, tr.first) + tr.lam >= av) continue;
+                        uint32_t tc;
+                        if (eu <= tr.first) {
+                            tc = tr.first;
+                        } else {
+                            tc = cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                            if (COUNT) {
+                                ++c_crec;
+                                const uint4 r0 = __ldg(ix.crec + 2ull * (tr.crec_base + eu / ix.cs - tr.c_first));
+                                if (r0.y == kItemSpill) c_spill += r0.w;
+                            }
+                        }
+                        const uint32_t cand = tc + tr.lam;
+                        if (cand < av) {
+                            const uint32_t old = atomicMin(arr + tr.v, cand);
+                            if (cand < old) {
+                                atomicOr(nxt + (tr.v >> 5), 1u << (tr.v & 31u));
+                                if (COUNT) ++c_impr;
+                            }
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            int any = 0;
+            for (uint32_t i = tid; i < W; i += kCtaThreads) {
+                cur[i] = 0;
+                any |= nxt[i] != 0u;
+            }
+            any = __syncthreads_or(any);
+            uint32_t *tmp = cur;
+            cur = nxt;
+            nxt = tmp;
+            ++sweeps;
+            if (!any) break;
+        }
+        // Output in caller ids
+        for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = varr[__ldg(ix.perm + i)];
+        if (tid == 0 && sweeps_out) sweeps_out[q] = sweeps;
+        if (COUNT) {
+            unsigned long long v[5] = {c_vis, c_type, c_crec, c_spill, c_impr};
+            for (int k = 0; k < 5; ++k) {
+                for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o);
+                if ((tid & 31u) == 0 && v[k]) atomicAdd(counters + k, v[k]);
+            }
+            if (tid == 0) atomicAdd(counters + 5, (unsigned long long)sweeps);
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- grid kernel
+// One query on the whole GPU: persistent cooperative grid, global e[],
+// one grid barrier per sweep.  SCHED == kSchedFrontier: the frontier is a
+// worklist (sub-warp per queued vertex, dedup by sweep stamps).
+// SCHED == kSchedFull: topology-driven full sweep, one thread per connection
+// type, active test on a bitmap (the paper's thread-per-type schedule,
+// PAPER.md:228, 305).
+constexpr int kGridThreads = 256;
+
+template <int SW, int SCHED>
+__global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWork w, uint32_t s, uint32_t ts,
+                                                             uint32_t *out) {
+    const uint32_t n = ix.n;
+    const uint32_t W = (n + 31u) / 32u;
+    const uint64_t gtid = blockIdx.x * uint64_t(kGridThreads) + threadIdx.x;
+    const uint64_t gsz = uint64_t(gridDim.x) * kGridThreads;
+    uint32_t *bar = w.ctl + 4;
+    // Initialize (Algorithm 2)
+    for (uint64_t i = gtid; i < n; i += gsz) {
+        w.arr[i] = kInf;
+        if (SCHED == kSchedFrontier) w.stamp[i] = 0;
+    }
+    if (SCHED == kSchedFull)
+        for (uint64_t i = gtid; i < 3ull * W; i += gsz) w.bm[i] = 0;
+    if (gtid == 0) {
+        w.ctl[0] = 1;  // sweep 0 sees one active vertex
+        w.ctl[1] = 0;
+        w.ctl[2] = 0;
+    }
+    grid_sync(bar);
+    if (gtid == 0) {
+        const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
+        w.arr[si] = ts;
+        if (SCHED == kSchedFrontier) w.q0[0] = si;
+        else w.bm[si >> 5] = 1u << (si & 31u);
+    }
+    grid_sync(bar);
+
+    uint32_t sweep = 0;
+    for (;;) {
+        const uint32_t c_cur = sweep % 3u, c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
+        if (gtid == 0) w.ctl[c_old] = 0;
+        if (SCHED == kSchedFrontier) {
+            const uint32_t cnt = ld_cg(w.ctl + c_cur);
+            const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
+            uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
+            const uint32_t lane = uint32_t(gtid % SW);
+            for (uint64_t it = gtid / SW; it < cnt; it += gsz / SW) {
+                const uint32_t x = ld_cg(qc + it);
+                const uint32_t eu = ld_cg(w.arr + x);
+                const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
+                for (uint32_t t = p0 + lane; t < p1; t += SW) {
+                    const TypeRec tr = load_type(ix, t);
+                    if (eu > tr.last) continue;
+                    const uint32_t av = ld_cg(w.arr + tr.v);
+                    if (max(eu, tr.first) + tr.lam >= av) continue;
+                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                    const uint32_t cand = tc + tr.lam;
+                    if (cand < av) {
+                        const uint32_t old = atomicMin(w.arr + tr.v, cand);
+                        if (cand < old && atomicExch(w.stamp + tr.v, sweep + 1u) != sweep + 1u)
+                            push_aggregated(tr.v, qn, w.ctl + c_nxt);
+                    }
+                }
+            }
+        } else {
+            const uint32_t *bc = w.bm + uint64_t(c_cur) * W;
+            uint32_t *bn = w.bm + uint64_t(c_nxt) * W;
+            uint32_t *bo = w.bm + uint64_t(c_old) * W;
+            for (uint64_t i = gtid; i < W; i += gsz) bo[i] = 0;
+            bool improved = false;
+            for (uint64_t t = gtid; t < ix.num_types; t += gsz) {
+                const uint32_t x = __ldg(ix.type_src + t);
+                if (!((ld_cg(bc + (x >> 5)) >> (x & 31u)) & 1u)) continue;
+                const uint32_t eu = ld_cg(w.arr + x);
+                const TypeRec tr = load_type(ix, t);
+                if (eu > tr.last) continue;
+                const uint32_t av = ld_cg(w.arr + tr.v);
+                if (max(eu, tr.first) + tr.lam >= av) continue;
+                const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                const uint32_t cand = tc + tr.lam;
+                if (cand < av) {
+                    const uint32_t old = atomicMin(w.arr + tr.v, cand);
+                    if (cand < old) {
+                        atomicOr(bn + (tr.v >> 5), 1u << (tr.v & 31u));
+                        improved = true;
+                    }
+                }
+            }
+            if (__any_sync(0xFFFFFFFFu, improved) && (threadIdx.x & 31u) == 0) atomicExch(w.ctl + c_nxt, 1u);
+        }
+        grid_sync(bar);
+        ++sweep;
+        if (ld_cg(w.ctl + c_nxt) == 0u) break;
+    }
+    for (uint64_t i = gtid; i < n; i += gsz) out[i] = ld_cg(w.arr + __ldg(ix.perm + i));
+    if (gtid == 0) w.ctl[8] = sweep;
+}
+
+template <int SW, bool COUNT>
+cudaError_t launch_cta_sw(const DevIndex &ix, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
+                          uint32_t *sweeps, unsigned long long *qc, unsigned long long *inv, int grid_cap,
+                          unsigned long long *counters, cudaStream_t st) {
+    const size_t smem = cta_smem_bytes(ix.n);
+    cudaError_t e = cudaFuncSetAttribute(k_query_cta<SW, COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<SW, COUNT>, kCtaThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    uint64_t grid = std::min<uint64_t>(uint64_t(sms) * per_sm, nq);
+    if (grid_cap > 0) grid = std::min<uint64_t>(grid, uint64_t(grid_cap));
+    if (grid == 0) return cudaSuccess;
+    e = cudaMemsetAsync(qc, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    k_query_cta<SW, COUNT><<<unsigned(grid), kCtaThreads, smem, st>>>(ix, src, ts, nq, out, sweeps, qc, inv, counters);
+    return cudaGetLastError();
+}
+
+template <int SW, int SCHED>
+cudaError_t launch_grid_sw(const DevIndex &ix, const GridWork &w, uint32_t s, uint32_t ts, uint32_t *out,
+                           cudaStream_t st) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_grid<SW, SCHED>, kGridThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    per_sm = std::min(per_sm, 4);
+    dim3 grid(unsigned(sms * per_sm)), block(kGridThreads);
+    e = cudaMemsetAsync(w.ctl + 4, 0, 2 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    DevIndex ixc = ix;
+    GridWork wc = w;
+    void *args[] = {&ixc, &wc, &s, &ts, &out};
+    return cudaLaunchCooperativeKernel((const void *)k_query_grid<SW, SCHED>, grid, block, args, 0, st);
+}
+
+}  // namespace
+
+size_t cta_smem_bytes(uint32_t n) {
+    const size_t npad = (n + 3u) & ~3u, W = (n + 31u) / 32u;
+    return (npad + 2 * W) * sizeof(uint32_t);
+}
+
+int cta_grid_size(uint32_t n, int subwarp) {
+    (void)subwarp;
+    int dev = 0, optin = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t need = cta_smem_bytes(n) + 64;
+    if (need > size_t(optin)) return 0;
+    cudaFuncSetAttribute(k_query_cta<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<8, false>, kCtaThreads, cta_smem_bytes(n));
+    return per_sm * sms;
+}
+
+cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,
+                          uint32_t *d_out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, 148ull * 32));
+    k_lookup<<<blocks, 256, 0, st>>>(ix, d_type, d_bound, n, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_src, const uint32_t *d_ts,
+                             uint64_t nq, uint32_t *d_out, uint32_t *d_sweeps, unsigned long long *d_qcounter,
+                             unsigned long long *d_invalid, int grid_cap, unsigned long long *d_counters,
+                             cudaStream_t st) {
+#define EAT_CTA_CASE(SWV)                                                                                     \
+    case SWV:                                                                                                 \
+        return d_counters ? launch_cta_sw<SWV, true>(ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter, d_invalid, \
+                                                     grid_cap, d_counters, st)                                \
+                          : launch_cta_sw<SWV, false>(ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter,        \
+                                                      d_invalid, grid_cap, nullptr, st);
+    switch (subwarp) {
+        EAT_CTA_CASE(1)
+        EAT_CTA_CASE(2)
+        EAT_CTA_CASE(4)
+        EAT_CTA_CASE(8)
+        EAT_CTA_CASE(16)
+        EAT_CTA_CASE(32)
+        default: return cudaErrorInvalidValue;
+    }
+#undef EAT_CTA_CASE
+}
+
+cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,
+                              uint32_t t_s, uint32_t *d_out, cudaStream_t st) {
+    if (sched == kSchedFull) return launch_grid_sw<1, kSchedFull>(ix, w, s, t_s, d_out, st);
+    switch (subwarp) {
+        case 1: return launch_grid_sw<1, kSchedFrontier>(ix, w, s, t_s, d_out, st);
+        case 2: return launch_grid_sw<2, kSchedFrontier>(ix, w, s, t_s, d_out, st);
+        case 4: return launch_grid_sw<4, kSchedFrontier>(ix, w, s, t_s, d_out, st);
+        case 8: return launch_grid_sw<8, kSchedFrontier>(ix, w, s, t_s, d_out, st);
+        case 16: return launch_grid_sw<16, kSchedFrontier>(ix, w, s, t_s, d_out, st);
+        case 32: return launch_grid_sw<32, kSchedFrontier>(ix, w, s, t_s, d_out, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace eat

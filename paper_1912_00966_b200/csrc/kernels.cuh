@@ -1,0 +1,53 @@
+// kernels.cuh -- launch interface of the sm_100a relaxation kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace eat {
+
+// Device view of the packed index (layout: eat_internal.h).
+struct DevIndex {
+    uint32_t n;                 // |V| (all vertices; a partition owns a sub-range of sources)
+    uint32_t cs;                // cluster seconds
+    uint64_t num_types;
+    const uint32_t *type_ptr;   // [n+1]
+    const uint4 *type_rec;      // [2*T]  (32 B per type)
+    const uint4 *crec;          // [2*R]  (32 B per cluster record)
+    const uint32_t *pool;       // spilled items
+    const uint32_t *type_src;   // [T] internal source vertex per type (full-sweep schedule)
+    const uint32_t *perm;       // [n] caller id -> internal id
+};
+
+// Scratch of the grid-wide persistent single-query kernel.
+struct GridWork {
+    uint32_t *arr;       // [n] arrival times, internal ids
+    uint32_t *q0, *q1;   // [n] frontier worklists (ping-pong)
+    uint32_t *stamp;     // [n] "queued for sweep k" stamps (dedup)
+    uint32_t *bm;        // [3*W] rotating active bitmaps (full-sweep schedule)
+    uint32_t *ctl;       // [16] control words: 0-2 rotating counters, 4-5 grid barrier, 8 sweeps
+};
+
+enum { kSchedFrontier = 0, kSchedFull = 1 };
+
+// Largest dynamic shared memory (bytes) the CTA kernel may use on `device`.
+size_t cta_smem_bytes(uint32_t n);
+
+// Cluster-AP lookup for (type, bound) pairs (test entry point).
+cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,
+                          uint32_t *d_out, cudaStream_t st);
+
+// One CTA per query, arr in shared memory.  d_qcounter: one uint64 zeroed here.
+// d_counters: NULL, or 6 uint64 work counters accumulated by the instrumented variant.
+cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_src, const uint32_t *d_ts,
+                             uint64_t nq, uint32_t *d_out, uint32_t *d_sweeps, unsigned long long *d_qcounter,
+                             unsigned long long *d_invalid, int grid_cap, unsigned long long *d_counters,
+                             cudaStream_t st);
+
+// Grid-wide persistent kernel for one query with global arr (cooperative launch).
+cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,
+                              uint32_t t_s, uint32_t *d_out, cudaStream_t st);
+
+// Occupancy-derived grid size of the CTA kernel for n vertices (0 if arr does not fit).
+int cta_grid_size(uint32_t n, int subwarp);
+
+}  // namespace eat

@@ -1,0 +1,137 @@
+"""Thin Python front end of libeat.so (argument marshalling only).
+
+``Engine(tt, ...)`` calls ``eat_build``; ``query`` / ``query_many`` call
+``eat_query`` / ``eat_query_many`` with host NumPy buffers; the ``*_device``
+methods take torch CUDA tensors (PyTorch is used for device memory and
+streams only).  Nothing here computes any part of the EAT path.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import EAT_INF
+
+
+def _u32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+
+
+def _p(a: Optional[np.ndarray], t=ctypes.c_uint32):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(t))
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Engine:
+    """A built EAT index on one device (or one edge partition of it)."""
+
+    def __init__(self, num_vertices: int, u, v, dep, dur, xy=None, *, cluster_seconds: int = 3600,
+                 renumber: str = "auto", kernel: str = "auto", subwarp: int = 8, device: int = -1,
+                 host_only: bool = False, counters: bool = False, mode: str = "replicated", part_rank: int = 0, part_count: int = 1,
+                 nccl_unique_id: Optional[bytes] = None):
+        self._h = None
+        arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
+        m = arrs[0].shape[0]
+        if any(a.shape[0] != m for a in arrs):
+            raise ValueError("u, v, dep, dur must have equal length")
+        xy_a = None if xy is None else np.ascontiguousarray(np.asarray(xy, dtype=np.float32).reshape(-1))
+        tt = _lib.eat_timetable(num_vertices=int(num_vertices), num_connections=int(m),
+                                u=_p(arrs[0]), v=_p(arrs[1]), dep=_p(arrs[2]), dur=_p(arrs[3]), trip=None,
+                                xy=_p(xy_a, ctypes.c_float))
+        self._nccl_buf = None
+        if nccl_unique_id is not None:
+            self._nccl_buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+        opts = _lib.eat_build_opts(cluster_seconds=int(cluster_seconds), renumber=_lib.EAT_RENUMBER[renumber],
+                                   device=int(device), kernel=_lib.EAT_KERNEL[kernel],
+                                   flags=(_lib.EAT_BUILD_HOST_ONLY if host_only else 0)
+                                   | (_lib.EAT_BUILD_COUNTERS if counters else 0), subwarp=int(subwarp),
+                                   mode=_lib.EAT_MODE[mode], part_rank=int(part_rank), part_count=int(part_count),
+                                   nccl_unique_id=ctypes.cast(self._nccl_buf, ctypes.c_void_p) if self._nccl_buf else None)
+        self._h = _lib.eat_build(tt, opts)
+        self.num_vertices = int(num_vertices)
+        self.num_connections = int(m)
+
+    @classmethod
+    def from_timetable(cls, tt, **kw) -> "Engine":
+        return cls(tt.num_vertices, tt.u, tt.v, tt.dep, tt.dur, getattr(tt, "xy", None), **kw)
+
+    # ------------------------------------------------------------------ lifecycle
+    def close(self):
+        if self._h is not None:
+            _lib.eat_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ------------------------------------------------------------------ queries
+    def query(self, s: int, t_s: int) -> np.ndarray:
+        out = np.empty(self.num_vertices, dtype=np.uint32)
+        _lib.eat_query(self._h, int(s), int(t_s), out.ctypes.data)
+        return out
+
+    def query_many(self, sources, times) -> np.ndarray:
+        src, ts = _u32(sources), _u32(times)
+        if src.shape != ts.shape:
+            raise ValueError("sources and times must have equal length")
+        out = np.empty((src.shape[0], self.num_vertices), dtype=np.uint32)
+        _lib.eat_query_many(self._h, src.ctypes.data, ts.ctypes.data, src.shape[0], out.ctypes.data)
+        return out
+
+    def query_device(self, s: int, t_s: int, out, stream=None):
+        """out: int32/uint32 CUDA tensor [num_vertices] on this engine's device."""
+        _lib.eat_query_device(self._h, int(s), int(t_s), out.data_ptr(), _stream_ptr(stream))
+        return out
+
+    def query_many_device(self, sources, times, out, stream=None):
+        """sources, times: int32 CUDA tensors [nq]; out: int32 CUDA tensor [nq, num_vertices]."""
+        nq = int(sources.numel())
+        _lib.eat_query_many_device(self._h, sources.data_ptr(), times.data_ptr(), nq, out.data_ptr(),
+                                   _stream_ptr(stream))
+        return out
+
+    def lookup_device(self, types, bounds, out, stream=None):
+        _lib.eat_lookup_device(self._h, types.data_ptr(), bounds.data_ptr(), int(types.numel()), out.data_ptr(),
+                               _stream_ptr(stream))
+        return out
+
+    def partition_range(self, rank: int, count: int):
+        """Internal-vertex range [lo, hi) owned by edge partition `rank` of `count`."""
+        return _lib.eat_partition_range(self._h, int(rank), int(count))
+
+    # ------------------------------------------------------------------ introspection
+    def stats(self) -> dict:
+        d = _lib.eat_get_stats(self._h).as_dict()
+        d["kernel_name"] = _lib.EAT_KERNEL_NAMES.get(d["kernel"], "?")
+        return d
+
+    def export(self) -> dict:
+        """Host copy of the packed index (layout documented in include/eat.h)."""
+        n = self.num_vertices
+        nt, nr, npool = _lib.eat_index_sizes(self._h)
+        perm = np.empty(n, dtype=np.uint32)
+        tptr = np.empty(n + 1, dtype=np.uint32)
+        trec = np.empty((max(nt, 1), 8), dtype=np.uint32)
+        crec = np.empty((max(nr, 1), 8), dtype=np.uint32)
+        pool = np.empty(max(npool, 1), dtype=np.uint32)
+        _lib.eat_index_export(self._h, perm.ctypes.data, tptr.ctypes.data, trec.ctypes.data, crec.ctypes.data,
+                              pool.ctypes.data)
+        return dict(perm=perm, type_ptr=tptr, type_rec=trec[:nt], crec=crec[:nr], pool=pool[:npool])

@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element
+by element, bit-exact (integer seconds; EAT_INF for unreachable).
+
+Run on a B200 via gpurun:  python -m pytest tests -m gpu -x -q
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import INF
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1912_00966_b200 import Engine, EatError, _lib  # noqa: E402
+
+KERNELS = ["cta", "frontier", "full_sweep"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _types_raw(tt):
+    """(u, v, lambda) -> sorted departures, from the RAW timetable (caller ids)."""
+    order = np.lexsort((tt.dep, tt.dur, tt.v, tt.u))
+    u, v, d, t = tt.u[order], tt.v[order], tt.dur[order], tt.dep[order]
+    key = np.stack([u, v, d], 1)
+    brk = np.nonzero(np.any(key[1:] != key[:-1], axis=1))[0] + 1
+    starts = np.concatenate([[0], brk])
+    ends = np.concatenate([brk, [len(u)]])
+    return {(int(u[a]), int(v[a]), int(d[a])): t[a:b] for a, b in zip(starts, ends)}
+
+
+def _assert_rows(got, want, what):
+    if not np.array_equal(got, want):
+        bad = np.nonzero(got != want)
+        i = tuple(x[0] for x in bad)
+        raise AssertionError(f"{what}: {len(bad[0])} mismatches, first at {i}: got {got[i]} want {want[i]}")
+
+
+# ----------------------------------------------------------------------------- lookup kernel
+@pytest.mark.parametrize("name,cs", [("tiny", 3600), ("tiny", 900), ("city", 3600)])
+def test_lookup_kernel_vs_get_connection(name, cs):
+    tt = synth.generate(name)
+    eng = Engine.from_timetable(tt, cluster_seconds=cs)
+    ex = eng.export()
+    inv = np.empty(tt.num_vertices, np.int64)
+    inv[ex["perm"].astype(np.int64)] = np.arange(tt.num_vertices)
+    raw = _types_raw(tt)
+    rng = np.random.default_rng(1)
+    T = ex["type_rec"].shape[0]
+    ts = rng.choice(T, min(T, 3000), replace=False)
+    types, bounds, want = [], [], []
+    for t in ts:
+        rec = ex["type_rec"][t]
+        deps = raw[(int(inv[rec[6]]), int(inv[rec[0]]), int(rec[1]))]
+        cand = np.concatenate([deps, deps + 1, deps - 1, [0, deps[-1] + 1, int(rng.integers(0, 100000))]])
+        cand = np.unique(cand[cand >= 0])
+        for b in cand:
+            g = oracle.get_connection(deps.tolist(), int(b))
+            types.append(t)
+            bounds.append(b)
+            want.append(INF if g is None else g)
+    dt = torch.tensor(np.array(types, np.int64).astype(np.int32), device="cuda")
+    db = torch.tensor(np.array(bounds, np.int64).astype(np.int32), device="cuda")
+    out = torch.empty_like(dt)
+    eng.lookup_device(dt, db, out)
+    torch.cuda.synchronize()
+    _assert_rows(out.cpu().numpy().astype(np.uint32), np.array(want, np.uint32), f"lookup {name} cs={cs}")
+
+
+# ----------------------------------------------------------------------------- single queries
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("subwarp", [1, 8, 32])
+def test_tiny_single_queries(kernel, subwarp):
+    tt = synth.generate("tiny")
+    eng = Engine.from_timetable(tt, kernel=kernel, subwarp=subwarp)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    rng = np.random.default_rng(subwarp)
+    qs = [synth.SINGLE_QUERY] + [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 90000))) for _ in range(30)]
+    for s, t_s in qs:
+        _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"tiny {kernel}/{subwarp} q=({s},{t_s})")
+    st = eng.stats()
+    assert st["kernel_name"] == kernel and st["last_sweeps"] >= 1
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_random_small_instances(kernel):
+    """>= 1000 (instance, query) pairs with lambda=0, duplicates, self-loops,
+    multi-day departures (SPEC S:348 engine-equivalence property)."""
+    npairs = 0
+    for seed in range(400 if kernel != "full_sweep" else 150):
+        tt = synth.random_small(seed)
+        eng = Engine.from_timetable(tt, kernel=kernel, cluster_seconds=[3600, 600, 4096, 60][seed % 4],
+                                    subwarp=[1, 2, 4, 8, 16, 32][seed % 6])
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        rng = np.random.default_rng(seed)
+        for _ in range(3):
+            s, t_s = int(rng.integers(tt.num_vertices)), int(rng.integers(0, 2 * 86400))
+            _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"seed {seed} {kernel} q=({s},{t_s})")
+            npairs += 1
+        eng.close()
+    assert npairs >= 450
+
+
+def test_edge_cases():
+    # one vertex, no connections
+    eng = Engine(1, [], [], [], [])
+    assert eng.query(0, 5).tolist() == [5]
+    # isolated source, late start, t_s = 0, t_s = INF-1
+    tt = synth.generate("tiny")
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    for kernel in KERNELS:
+        eng = Engine.from_timetable(tt, kernel=kernel)
+        for s, t_s in [(0, 0), (0, 200000), (5, INF - 1), (199, 86399)]:
+            _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"edge {kernel} ({s},{t_s})")
+        with pytest.raises(EatError) as e:
+            eng.query(tt.num_vertices, 0)
+        assert e.value.status == _lib.EAT_EINVAL
+        with pytest.raises(EatError) as e:
+            eng.query(0, INF)
+        assert e.value.status == _lib.EAT_ERANGE
+
+
+def test_query_device_and_stream():
+    tt = synth.generate("tiny")
+    eng = Engine.from_timetable(tt)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    out = torch.empty(tt.num_vertices, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        eng.query_device(3, 30000, out, stream=s)
+    s.synchronize()
+    _assert_rows(out.cpu().numpy().astype(np.uint32), csa.query(3, 30000), "query_device")
+
+
+# ----------------------------------------------------------------------------- batched
+def test_tiny_batched_all_rows():
+    tt = synth.generate("tiny")
+    eng = Engine.from_timetable(tt)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    src, ts = synth.queries(tt, 100, 10)
+    _assert_rows(eng.query_many(src, ts), csa.query_many(src, ts), "tiny batch host")
+    d_src = torch.tensor(src.astype(np.int32), device="cuda")
+    d_ts = torch.tensor(ts.astype(np.int32), device="cuda")
+    out = torch.empty((src.size, tt.num_vertices), dtype=torch.int32, device="cuda")
+    eng.query_many_device(d_src, d_ts, out)
+    torch.cuda.synchronize()
+    _assert_rows(out.cpu().numpy().astype(np.uint32), csa.query_many(src, ts), "tiny batch device")
+
+
+def test_batched_invalid_rows_on_device():
+    tt = synth.generate("tiny")
+    eng = Engine.from_timetable(tt)
+    d_src = torch.tensor([0, tt.num_vertices + 3, 1], dtype=torch.int32, device="cuda")
+    d_ts = torch.tensor([100, 100, -1], dtype=torch.int32, device="cuda")  # -1 -> 0xFFFFFFFF >= INF
+    out = torch.zeros((3, tt.num_vertices), dtype=torch.int32, device="cuda")
+    eng.query_many_device(d_src, d_ts, out)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy().astype(np.uint32)
+    assert np.all(o[1] == INF) and np.all(o[2] == INF) and o[0][0] == 100
+    assert eng.stats()["invalid_queries"] >= 2
+
+
+def test_city_batch_full_size_sampled():
+    """BASELINE configs[2]: city network, 10k queries (1000 sources x 10
+    times, seed 7) in the bench's launch configuration; 120 sampled rows
+    compared with the oracle one by one."""
+    tt = synth.generate("city")
+    eng = Engine.from_timetable(tt)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    src, ts = synth.queries(tt, 1000, 10)
+    d_src = torch.tensor(src.astype(np.int32), device="cuda")
+    d_ts = torch.tensor(ts.astype(np.int32), device="cuda")
+    out = torch.empty((src.size, tt.num_vertices), dtype=torch.int32, device="cuda")
+    eng.query_many_device(d_src, d_ts, out)
+    torch.cuda.synchronize()
+    rows = np.random.default_rng(7).choice(src.size, 120, replace=False)
+    got = out[torch.tensor(rows, device="cuda")].cpu().numpy().astype(np.uint32)
+    _assert_rows(got, csa.query_many(src[rows], ts[rows]), "city batch sampled rows")
+    # host e2e path on a slice
+    _assert_rows(eng.query_many(src[:200], ts[:200]), csa.query_many(src[:200], ts[:200]), "city batch host")
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_city_single_query(kernel):
+    """BASELINE configs[1]: s=0, t_s=06:00, plus 10 seeded queries."""
+    tt = synth.generate("city")
+    eng = Engine.from_timetable(tt, kernel=kernel)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    rng = np.random.default_rng(11)
+    qs = [synth.SINGLE_QUERY] + [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 86400))) for _ in range(10)]
+    for s, t_s in qs:
+        _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"city {kernel} ({s},{t_s})")
+
+
+def test_metro_single_query():
+    """BASELINE configs[3]: metro network, global e[] (frontier kernel)."""
+    tt = synth.generate("metro")
+    eng = Engine.from_timetable(tt)
+    assert eng.stats()["kernel_name"] in ("frontier", "cta")
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    for s, t_s in [synth.SINGLE_QUERY, (777, 30000)]:
+        _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"metro ({s},{t_s})")
+
+
+# ----------------------------------------------------------------------------- edge partition
+def test_edge_partitioned_single_rank():
+    tt = synth.generate("tiny")
+    eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=1)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    for s, t_s in [synth.SINGLE_QUERY, (17, 40000)]:
+        _assert_rows(eng.query(s, t_s), csa.query(s, t_s), "edge-partitioned P=1")
+    assert eng.stats()["last_rounds"] == 1
