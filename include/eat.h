@@ -109,7 +109,13 @@ typedef struct eat_build_opts {
     uint32_t part_rank;           /* EDGE_PARTITIONED: this process's rank */
     uint32_t part_count;          /* EDGE_PARTITIONED: number of ranks (1 = single partition) */
     const void *nccl_unique_id;   /* EDGE_PARTITIONED with part_count > 1: 128-byte ncclUniqueId, same on every rank */
+    uint32_t window_seconds;      /* CTA-kernel schedule: a sweep relaxes the active vertices with
+                                     e[u] <= min_active(e) + window (others stay active); EAT_INF = every
+                                     active vertex (the paper's schedule); 0 -> EAT_DEFAULT_WINDOW.
+                                     Results are identical for every value (same fixpoint). */
 } eat_build_opts;
+
+#define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */
 
 typedef struct eat_handle eat_handle;
 

@@ -53,6 +53,16 @@ cudaError_t dalloc_copy(T **dst, const T *src, size_t count, size_t &bytes) {
 
 }  // namespace
 
+// One uploaded slice of the packed index: the out-types of internal
+// sources [lo, hi) (everything for a replicated handle).
+struct Slice {
+    uint32_t lo = 0, hi = 0;
+    uint32_t *type_ptr = nullptr, *type_rec = nullptr, *crec = nullptr, *pool = nullptr, *type_src = nullptr;
+    eat::DevIndex ix{};
+    eat::PartWork pw{};
+    uint64_t num_crec = 0, num_pool = 0;
+};
+
 struct eat_handle {
     std::mutex mu;
     eat::HostIndex hx;
@@ -61,12 +71,15 @@ struct eat_handle {
     uint32_t kernel = EAT_KERNEL_AUTO;   // resolved single-query kernel
     uint32_t subwarp = 8;
     uint32_t mode = EAT_MODE_REPLICATED;
+    uint32_t window = EAT_INF;           // CTA schedule time window (EAT_INF = all active vertices)
     cudaStream_t stream = nullptr;
-    // device index
-    uint32_t *d_type_ptr = nullptr, *d_type_rec = nullptr, *d_crec = nullptr, *d_pool = nullptr;
-    uint32_t *d_type_src = nullptr, *d_perm = nullptr;
-    eat::DevIndex ix{};
+    // device index: slices[0] is this handle's index (whole, or its own edge
+    // partition); a loopback edge-partitioned handle holds all P partitions
+    std::vector<Slice> slices;
+    uint32_t *d_perm = nullptr;
+    eat::DevIndex ix{};   // == slices[0].ix
     size_t index_bytes = 0;
+    bool loopback = false;
     // single-query scratch
     eat::GridWork gw{};
     uint32_t *d_out1 = nullptr, *h_out1 = nullptr;
@@ -81,7 +94,6 @@ struct eat_handle {
     // edge partition
     uint32_t part_rank = 0, part_count = 1, part_lo = 0, part_hi = 0;
     ncclComm_t comm = nullptr;
-    eat::PartWork pw{};
     // stats
     eat_stats st{};
 };
@@ -91,26 +103,29 @@ namespace {
 void release_device(eat_handle *h) {
     if (h->host_only) return;
     cudaSetDevice(h->device);
-    void *ptrs[] = {h->d_type_ptr, h->d_type_rec, h->d_crec, h->d_pool, h->d_type_src, h->d_perm,
-                    h->gw.arr,     h->gw.q0,      h->gw.q1,  h->gw.stamp, h->gw.bm,  h->gw.ctl,
-                    h->d_out1,     h->d_q1,       h->d_sweeps1, h->d_counter, h->d_invalid, h->d_bsrc,
-                    h->d_bts,      h->d_bout,     h->d_work};
+    void *ptrs[] = {h->d_perm,  h->gw.arr, h->gw.q0,     h->gw.q1,      h->gw.stamp,   h->gw.bm,
+                    h->gw.ctl,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
+                    h->d_bsrc,  h->d_bts,  h->d_bout,    h->d_work};
     for (void *p : ptrs)
         if (p) cudaFree(p);
-    eat::part_free(h->pw);
+    for (Slice &sl : h->slices) {
+        void *sp[] = {sl.type_ptr, sl.type_rec, sl.crec, sl.pool, sl.type_src};
+        for (void *p : sp)
+            if (p) cudaFree(p);
+        eat::part_free(sl.pw);
+    }
     if (h->h_out1) cudaFreeHost(h->h_out1);
     if (h->comm) ncclCommDestroy(h->comm);
     if (h->stream) cudaStreamDestroy(h->stream);
 }
 
-eat_status upload(eat_handle *h) {
+// Upload the out-types of internal sources [lo, hi) as one slice (offsets
+// rebased to the slice).  type_ptr keeps all n+1 entries (empty outside).
+eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     const eat::HostIndex &x = h->hx;
     const uint32_t n = x.n;
-    // Slice of the index owned by this partition: sources [lo, hi).
-    uint32_t lo = 0, hi = n;
-    if (h->mode == EAT_MODE_EDGE_PARTITIONED) eat::partition_range(x, h->part_rank, h->part_count, lo, hi);
-    h->part_lo = lo;
-    h->part_hi = hi;
+    sl.lo = lo;
+    sl.hi = hi;
     const uint32_t t_lo = x.type_ptr[lo], t_hi = x.type_ptr[hi];
     const uint64_t T = t_hi - t_lo;
     uint64_t r_lo = 0, r_hi = 0, p_lo = 0, p_hi = 0;
@@ -143,24 +158,46 @@ eat_status upload(eat_handle *h) {
     for (uint64_t r = 0; r < r_hi - r_lo; ++r)
         if (crec[r * eat::kCrecWords + 1] == eat::kItemSpill) crec[r * eat::kCrecWords + 2] -= uint32_t(p_lo);
     size_t &b = h->index_bytes;
-    CUDA_TRY(dalloc_copy(&h->d_type_ptr, tptr.data(), tptr.size(), b));
-    CUDA_TRY(dalloc_copy(&h->d_type_rec, trec.data(), trec.size(), b));
-    CUDA_TRY(dalloc_copy(&h->d_crec, crec.data(), crec.size(), b));
-    CUDA_TRY(dalloc_copy(&h->d_pool, x.pool.data() + p_lo, p_hi - p_lo, b));
-    CUDA_TRY(dalloc_copy(&h->d_type_src, tsrc.data(), tsrc.size(), b));
-    CUDA_TRY(dalloc_copy(&h->d_perm, x.perm.data(), x.perm.size(), b));
-    h->ix.n = n;
-    h->ix.cs = x.cs;
-    h->ix.num_types = T;
-    h->ix.type_ptr = h->d_type_ptr;
-    h->ix.type_rec = reinterpret_cast<const uint4 *>(h->d_type_rec);
-    h->ix.crec = reinterpret_cast<const uint4 *>(h->d_crec);
-    h->ix.pool = h->d_pool;
-    h->ix.type_src = h->d_type_src;
-    h->ix.perm = h->d_perm;
-    h->st.num_types = T;
-    h->st.num_cluster_records = r_hi - r_lo;
-    h->st.num_spill_items = p_hi - p_lo;
+    CUDA_TRY(dalloc_copy(&sl.type_ptr, tptr.data(), tptr.size(), b));
+    CUDA_TRY(dalloc_copy(&sl.type_rec, trec.data(), trec.size(), b));
+    CUDA_TRY(dalloc_copy(&sl.crec, crec.data(), crec.size(), b));
+    CUDA_TRY(dalloc_copy(&sl.pool, x.pool.data() + p_lo, p_hi - p_lo, b));
+    CUDA_TRY(dalloc_copy(&sl.type_src, tsrc.data(), tsrc.size(), b));
+    sl.ix.n = n;
+    sl.ix.cs = x.cs;
+    sl.ix.window = h->window;
+    sl.ix.num_types = T;
+    sl.ix.type_ptr = sl.type_ptr;
+    sl.ix.type_rec = reinterpret_cast<const uint4 *>(sl.type_rec);
+    sl.ix.crec = reinterpret_cast<const uint4 *>(sl.crec);
+    sl.ix.pool = sl.pool;
+    sl.ix.type_src = sl.type_src;
+    sl.ix.perm = h->d_perm;
+    sl.num_crec = r_hi - r_lo;
+    sl.num_pool = p_hi - p_lo;
+    return EAT_OK;
+}
+
+eat_status upload(eat_handle *h) {
+    const eat::HostIndex &x = h->hx;
+    const uint32_t n = x.n;
+    CUDA_TRY(dalloc_copy(&h->d_perm, x.perm.data(), x.perm.size(), h->index_bytes));
+    uint32_t nslices = h->loopback ? h->part_count : 1;
+    h->slices.resize(nslices);
+    for (uint32_t r = 0; r < nslices; ++r) {
+        uint32_t lo = 0, hi = n;
+        if (h->mode == EAT_MODE_EDGE_PARTITIONED)
+            eat::partition_range(x, h->loopback ? r : h->part_rank, h->part_count, lo, hi);
+        eat_status e = upload_slice(h, lo, hi, h->slices[r]);
+        if (e != EAT_OK) return e;
+    }
+    const Slice &s0 = h->slices[0];
+    h->ix = s0.ix;
+    h->part_lo = s0.lo;
+    h->part_hi = s0.hi;
+    h->st.num_types = s0.ix.num_types;
+    h->st.num_cluster_records = s0.num_crec;
+    h->st.num_spill_items = s0.num_pool;
     h->st.index_bytes = h->index_bytes;
     // scratch
     const uint64_t W = (n + 31ull) / 32ull;
@@ -175,9 +212,42 @@ eat_status upload(eat_handle *h) {
     CUDA_TRY(cudaMallocHost(&h->h_out1, n * 4ull + 64));
     CUDA_TRY(cudaMalloc(&h->d_q1, 2 * 4));
     CUDA_TRY(cudaMalloc(&h->d_sweeps1, 4));
+    CUDA_TRY(cudaMemset(h->d_sweeps1, 0, 4));
     CUDA_TRY(cudaMalloc(&h->d_counter, 8));
     CUDA_TRY(cudaMalloc(&h->d_invalid, 8));
     CUDA_TRY(cudaMemset(h->d_invalid, 0, 8));
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
+        for (Slice &sl : h->slices)
+            if (eat::part_alloc(sl.pw, n) != cudaSuccess) return fail(EAT_ENOMEM, "cannot allocate partition scratch");
+    return EAT_OK;
+}
+
+// Edge-partitioned query on this handle: NCCL ranks, or all partitions of a
+// loopback handle on one device.
+eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_out, cudaStream_t st) {
+    uint32_t rounds = 0, sweeps = 0;
+    eat_status e;
+    if (h->loopback) {
+        std::vector<eat::DevIndex> ixs;
+        std::vector<eat::PartWork *> ws;
+        std::vector<uint32_t> lo, hi;
+        for (Slice &sl : h->slices) {
+            ixs.push_back(sl.ix);
+            ws.push_back(&sl.pw);
+            lo.push_back(sl.lo);
+            hi.push_back(sl.hi);
+        }
+        e = eat::part_query_loopback(ixs, ws, lo, hi, int(h->subwarp), s, t_s, d_out, st, &rounds, &sweeps, g_err);
+    } else {
+        Slice &sl = h->slices[0];
+        e = eat::part_query(sl.ix, sl.pw, h->comm, sl.lo, sl.hi, int(h->subwarp), s, t_s, d_out, st, &rounds,
+                            &sweeps, g_err);
+    }
+    if (e != EAT_OK) return e;
+    h->st.last_rounds = rounds;
+    h->h_out1[h->hx.n] = sweeps;  // staged for d_sweeps1
+    CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->h_out1 + h->hx.n, 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     return EAT_OK;
 }
 
@@ -187,7 +257,8 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    h->st.smem_vertices_max = uint32_t((size_t(optin) - 64) * 32 / (4 * 32 + 2 * 4));
+    const size_t avail = size_t(optin) - eat::cta_static_smem() - 64;
+    h->st.smem_vertices_max = uint32_t(avail * 32 / (4 * 32 + 2 * 4));
     uint32_t k = requested;
     if (k == EAT_KERNEL_AUTO) k = h->cta_grid > 0 ? EAT_KERNEL_CTA : EAT_KERNEL_FRONTIER;
     if (k == EAT_KERNEL_CTA && h->cta_grid == 0)
@@ -244,14 +315,16 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
     if (o.kernel > EAT_KERNEL_CTA) return fail(EAT_EINVAL, "unknown kernel");
     uint32_t pc = o.part_count ? o.part_count : 1;
-    if (o.mode == EAT_MODE_EDGE_PARTITIONED && (o.part_rank >= pc || (pc > 1 && !o.nccl_unique_id)))
-        return fail(EAT_EINVAL, "edge partition needs part_rank < part_count and an NCCL unique id");
+    if (o.mode == EAT_MODE_EDGE_PARTITIONED && o.part_rank >= pc)
+        return fail(EAT_EINVAL, "edge partition needs part_rank < part_count");
     eat_handle *h = new (std::nothrow) eat_handle();
     if (!h) return fail(EAT_ENOMEM, "out of host memory");
     h->subwarp = sw;
     h->mode = o.mode;
+    h->window = o.window_seconds == 0 ? EAT_DEFAULT_WINDOW : o.window_seconds;
     h->part_rank = o.part_rank;
     h->part_count = pc;
+    h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 && !o.nccl_unique_id;
     h->host_only = (o.flags & EAT_BUILD_HOST_ONLY) != 0;
     std::string msg;
     int rc;
@@ -311,7 +384,7 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
                 break;
             }
         }
-        if (h->mode == EAT_MODE_EDGE_PARTITIONED) {
+        if (h->mode == EAT_MODE_EDGE_PARTITIONED && !h->loopback) {
             if (pc > 1) {
                 ncclUniqueId id;
                 std::memcpy(&id, o.nccl_unique_id, sizeof(id));
@@ -320,10 +393,6 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
                     est = fail(EAT_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
                     break;
                 }
-            }
-            if (eat::part_alloc(h->pw, h->hx.n) != cudaSuccess) {
-                est = fail(EAT_ENOMEM, "cannot allocate partition scratch");
-                break;
             }
         }
     } while (0);
@@ -378,14 +447,7 @@ eat_status eat_query_device(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_TRY(cudaSetDevice(h->device));
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    if (h->mode == EAT_MODE_EDGE_PARTITIONED) {
-        uint32_t rounds = 0, sweeps = 0;
-        e = eat::part_query(h->ix, h->pw, h->comm, h->part_lo, h->part_hi, int(h->subwarp), s, t_s, d_out, st,
-                            &rounds, &sweeps, g_err);
-        h->st.last_rounds = rounds;
-        CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, &h->pw.h_sweeps, 4, cudaMemcpyHostToDevice, st));
-        return e;
-    }
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED) return run_partitioned(h, s, t_s, d_out, st);
     return enqueue_single(h, s, t_s, d_out, st);
 }
 
@@ -396,12 +458,8 @@ eat_status eat_query(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *out_arr)
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_TRY(cudaSetDevice(h->device));
     if (h->mode == EAT_MODE_EDGE_PARTITIONED) {
-        uint32_t rounds = 0, sweeps = 0;
-        e = eat::part_query(h->ix, h->pw, h->comm, h->part_lo, h->part_hi, int(h->subwarp), s, t_s, h->d_out1,
-                            h->stream, &rounds, &sweeps, g_err);
+        e = run_partitioned(h, s, t_s, h->d_out1, h->stream);
         if (e != EAT_OK) return e;
-        h->st.last_rounds = rounds;
-        CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, &h->pw.h_sweeps, 4, cudaMemcpyHostToDevice, h->stream));
     } else {
         e = enqueue_single(h, s, t_s, h->d_out1, h->stream);
         if (e != EAT_OK) return e;

@@ -39,14 +39,22 @@ __device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t 
     const uint32_t r = crec_base + (k - c_first);
     const uint4 r0 = __ldg(ix.crec + 2ull * r);
     const uint32_t x = eu - k * ix.cs;
-    uint32_t best;
+    uint32_t best = kNone;
     if (r0.y == kItemSpill) {
-        best = kNone;
-        for (uint32_t i = 0; i < r0.w; ++i) best = min(best, item_next(__ldg(ix.pool + r0.z + i), x));
+        for (uint32_t i = 0; i < r0.w; ++i) {
+            const uint32_t it = __ldg(ix.pool + r0.z + i);
+            best = min(best, item_next(it, x));
+            if ((it & 0xFFFu) >= x) break;  // items sorted by first term: later ones start later
+        }
     } else {
         const uint4 r1 = __ldg(ix.crec + 2ull * r + 1);
-        best = min(min(item_next(r0.y, x), item_next(r0.z, x)), min(item_next(r0.w, x), item_next(r1.x, x)));
-        best = min(best, min(min(item_next(r1.y, x), item_next(r1.z, x)), item_next(r1.w, x)));
+        const uint32_t items[kInlineItems] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+        for (int i = 0; i < kInlineItems; ++i) {
+            if (items[i] == kItemEmpty) break;  // slots are filled from the front
+            best = min(best, item_next(items[i], x));
+            if ((items[i] & 0xFFFu) >= x) break;
+        }
     }
     return best != kNone ? k * ix.cs + best : r0.x;
 }

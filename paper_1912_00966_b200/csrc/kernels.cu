@@ -40,19 +40,33 @@ __global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *boun
 // barriers, and relaxation is chaotic inside a sweep (updates are visible at
 // once; a vertex lowered after it was read is re-marked).
 // Queries are taken dynamically from a global counter (persistent grid).
+//
+// One sweep (three CTA barriers):
+//   1. select + compact: every thread scans its bitmap words; an active
+//      vertex is selected when e[u] <= base + window (window = EAT_INF: all
+//      of them, the paper's schedule; base = min e[] over the frontier,
+//      tracked incrementally); selected vertices are appended to s_list by
+//      shared-memory atomics (order is irrelevant), the rest stay active;
+//   2. warp-level flattening: each warp takes 32 listed vertices, scans their
+//      type counts with shuffles and evaluates the (vertex, type) pairs 32 at
+//      a time (owner lane found by a 5-step shuffle search) -- all lanes busy,
+//      no per-vertex divergence, no block scan;
+//   3. next frontier = improved (nxt) + deferred (cur).
 constexpr int kCtaThreads = 512;
+constexpr int kCtaWarps = kCtaThreads / 32;
+constexpr uint32_t kListCap = 2048;  // selected vertices per sweep (overflow stays active)
 
 // COUNT: instrumented variant (EAT_BUILD_COUNTERS) accumulating, per launch,
 // the work counters used for algorithmic-byte accounting:
 // counters[0] vertex visits, [1] type records read, [2] cluster records read,
 // [3] spilled items read, [4] improvements (successful atomicMin), [5] sweeps.
-template <int SW, bool COUNT>
-__global__ void __launch_bounds__(kCtaThreads) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
-                                                            const uint32_t *__restrict__ tsv, uint64_t nq,
-                                                            uint32_t *__restrict__ out, uint32_t *sweeps_out,
-                                                            unsigned long long *qcounter,
-                                                            unsigned long long *invalid,
-                                                            unsigned long long *counters) {
+template <bool COUNT>
+__global__ void __launch_bounds__(kCtaThreads, 4) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
+                                                               const uint32_t *__restrict__ tsv, uint64_t nq,
+                                                               uint32_t *__restrict__ out, uint32_t *sweeps_out,
+                                                               unsigned long long *qcounter,
+                                                               unsigned long long *invalid,
+                                                               unsigned long long *counters) {
     extern __shared__ uint32_t sm[];
     const uint32_t n = ix.n;
     const uint32_t W = (n + 31u) / 32u;
@@ -61,9 +75,12 @@ __global__ void __launch_bounds__(kCtaThreads) k_query_cta(DevIndex ix, const ui
     volatile uint32_t *varr = sm;
     uint32_t *bmA = sm + npad;
     uint32_t *bmB = bmA + W;
+    __shared__ uint32_t s_list[kListCap];
+    __shared__ uint32_t s_cnt;
+    __shared__ uint32_t s_tmin[2];
     __shared__ unsigned long long s_q;
-    const uint32_t tid = threadIdx.x;
-    const uint32_t lane = tid % SW, sub = tid / SW, nsub = kCtaThreads / SW;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+    const uint32_t window = ix.window;
 
     for (;;) {
         if (tid == 0) s_q = atomicAdd(qcounter, 1ull);
@@ -87,6 +104,11 @@ __global__ void __launch_bounds__(kCtaThreads) k_query_cta(DevIndex ix, const ui
             bmA[i] = 0;
             bmB[i] = 0;
         }
+        if (tid == 0) {
+            s_cnt = 0;
+            s_tmin[0] = ts;
+            s_tmin[1] = kInf;
+        }
         __syncthreads();
         if (tid == 0) {
             const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
@@ -98,48 +120,126 @@ __global__ void __launch_bounds__(kCtaThreads) k_query_cta(DevIndex ix, const ui
         uint32_t sweeps = 0;
         uint32_t c_vis = 0, c_type = 0, c_crec = 0, c_spill = 0, c_impr = 0;
         for (;;) {
-            for (uint32_t wi = sub; wi < W; wi += nsub) {
-                uint32_t word = cur[wi];
-                while (word) {
-                    const uint32_t b = __ffs(word) - 1u;
-                    word &= word - 1u;
-                    const uint32_t x = wi * 32u + b;
-                    const uint32_t eu = varr[x];
-                    const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
-                    if (COUNT && lane == 0) ++c_vis;
-                    for (uint32_t t = p0 + lane; t < p1; t += SW) {
-                        const TypeRec tr = load_type(ix, t);
-                        if (COUNT) ++c_type;
-                        if (eu > tr.last) continue;
-                        const uint32_t av = varr[tr.v];
-                        if (max(eu, tr.first) + tr.lam >= av) continue;
-                        uint32_t tc;
-                        if (eu <= tr.first) {
-                            tc = tr.first;
-                        } else {
-                            tc = cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
-                            if (COUNT) {
-                                ++c_crec;
-                                const uint4 r0 = __ldg(ix.crec + 2ull * (tr.crec_base + eu / ix.cs - tr.c_first));
-                                if (r0.y == kItemSpill) c_spill += r0.w;
-                            }
+            const uint32_t nb = (sweeps + 1u) & 1u;  // s_tmin slot written by this sweep
+            uint32_t thr = kInf;
+            if (window < kInf) {
+                const uint32_t base = s_tmin[sweeps & 1u];
+                thr = base + min(window, kInf - base);  // saturating
+            }
+            // ---- 1. select + compact
+            uint32_t dmin = kInf;
+            for (uint32_t w = tid; w < W; w += kCtaThreads) {
+                const uint32_t word = cur[w];
+                if (!word) continue;
+                uint32_t sel = word;
+                if (thr < kInf) {
+                    sel = 0;
+                    uint32_t rest = word;
+                    while (rest) {
+                        const uint32_t b = __ffs(rest) - 1u;
+                        rest &= rest - 1u;
+                        const uint32_t a = varr[w * 32u + b];
+                        if (a <= thr) sel |= 1u << b;
+                        else dmin = min(dmin, a);
+                    }
+                }
+                const uint32_t k = __popc(sel);
+                if (!k) continue;
+                const uint32_t pos = atomicAdd(&s_cnt, k);
+                uint32_t put = pos < kListCap ? min(k, kListCap - pos) : 0u;
+                uint32_t taken = 0, rest = sel;
+                for (uint32_t i = 0; i < put; ++i) {
+                    const uint32_t b = __ffs(rest) - 1u;
+                    rest &= rest - 1u;
+                    s_list[pos + i] = w * 32u + b;
+                    taken |= 1u << b;
+                }
+                while (rest) {  // list full: stays active for a later sweep
+                    const uint32_t b = __ffs(rest) - 1u;
+                    rest &= rest - 1u;
+                    dmin = min(dmin, varr[w * 32u + b]);
+                }
+                cur[w] = word & ~taken;
+            }
+            dmin = __reduce_min_sync(0xFFFFFFFFu, dmin);
+            if (lane == 0 && dmin < kInf) atomicMin(&s_tmin[nb], dmin);
+            __syncthreads();
+            const uint32_t F = min(s_cnt, kListCap);
+            // ---- 2. warp-level flattened (vertex, type) pairs; a warp takes g
+            // consecutive list entries so that small frontiers still spread
+            // over all warps
+            const uint32_t g = min(32u, max(1u, (F + kCtaWarps - 1u) / kCtaWarps));
+            for (uint32_t k0 = wid * g; k0 < F; k0 += kCtaWarps * g) {
+                const uint32_t j = k0 + lane;
+                uint32_t x = 0, p0 = 0, nt = 0;
+                if (lane < g && j < F) {
+                    x = s_list[j];
+                    p0 = __ldg(ix.type_ptr + x);
+                    nt = __ldg(ix.type_ptr + x + 1) - p0;
+                    if (COUNT) ++c_vis;
+                }
+                uint32_t incl = nt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= uint32_t(o)) incl += y;
+                }
+                const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                for (uint32_t base = 0; base < tot; base += 32u) {
+                    const uint32_t qp = base + lane;
+                    // owner lane: smallest L with incl[L] > qp
+                    uint32_t L = 0;
+#pragma unroll
+                    for (uint32_t step = 16; step > 0; step >>= 1) {
+                        const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, L + step - 1u);
+                        if (v <= qp) L += step;
+                    }
+                    const uint32_t o_incl = __shfl_sync(0xFFFFFFFFu, incl, L);
+                    const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
+                    const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
+                    const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
+                    if (qp >= tot) continue;
+                    const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
+                    const uint32_t eu = varr[u];
+                    const TypeRec tr = load_type(ix, t);
+                    if (COUNT) ++c_type;
+                    if (eu > tr.last) continue;
+                    const uint32_t av = varr[tr.v];
+                    if (max(eu, tr.first) + tr.lam >= av) continue;
+                    uint32_t tc;
+                    if (eu <= tr.first) {
+                        tc = tr.first;
+                    } else {
+                        tc = cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                        if (COUNT) {
+                            ++c_crec;
+                            const uint4 rr = __ldg(ix.crec + 2ull * (tr.crec_base + eu / ix.cs - tr.c_first));
+                            if (rr.y == kItemSpill) c_spill += rr.w;
                         }
-                        const uint32_t cand = tc + tr.lam;
-                        if (cand < av) {
-                            const uint32_t old = atomicMin(arr + tr.v, cand);
-                            if (cand < old) {
-                                atomicOr(nxt + (tr.v >> 5), 1u << (tr.v & 31u));
-                                if (COUNT) ++c_impr;
-                            }
+                    }
+                    const uint32_t cand = tc + tr.lam;
+                    if (cand < av) {
+                        const uint32_t old = atomicMin(arr + tr.v, cand);
+                        if (cand < old) {
+                            atomicOr(nxt + (tr.v >> 5), 1u << (tr.v & 31u));
+                            if (window < kInf) atomicMin(&s_tmin[nb], cand);
+                            if (COUNT) ++c_impr;
                         }
                     }
                 }
             }
             __syncthreads();
+            // ---- 3. next frontier = improved + deferred
             int any = 0;
             for (uint32_t i = tid; i < W; i += kCtaThreads) {
+                const uint32_t v = nxt[i] | cur[i];
+                nxt[i] = v;
                 cur[i] = 0;
-                any |= nxt[i] != 0u;
+                any |= v != 0u;
+            }
+            if (tid == 0) {
+                s_cnt = 0;
+                s_tmin[sweeps & 1u] = kInf;  // slot for the sweep after next
             }
             any = __syncthreads_or(any);
             uint32_t *tmp = cur;
@@ -155,7 +255,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_query_cta(DevIndex ix, const ui
             unsigned long long v[5] = {c_vis, c_type, c_crec, c_spill, c_impr};
             for (int k = 0; k < 5; ++k) {
                 for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o);
-                if ((tid & 31u) == 0 && v[k]) atomicAdd(counters + k, v[k]);
+                if (lane == 0 && v[k]) atomicAdd(counters + k, v[k]);
             }
             if (tid == 0) atomicAdd(counters + 5, (unsigned long long)sweeps);
         }
@@ -262,17 +362,17 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     if (gtid == 0) w.ctl[8] = sweep;
 }
 
-template <int SW, bool COUNT>
+template <bool COUNT>
 cudaError_t launch_cta_sw(const DevIndex &ix, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
                           uint32_t *sweeps, unsigned long long *qc, unsigned long long *inv, int grid_cap,
                           unsigned long long *counters, cudaStream_t st) {
     const size_t smem = cta_smem_bytes(ix.n);
-    cudaError_t e = cudaFuncSetAttribute(k_query_cta<SW, COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = cudaFuncSetAttribute(k_query_cta<COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<SW, COUNT>, kCtaThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<COUNT>, kCtaThreads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = std::min<uint64_t>(uint64_t(sms) * per_sm, nq);
@@ -280,7 +380,7 @@ cudaError_t launch_cta_sw(const DevIndex &ix, const uint32_t *src, const uint32_
     if (grid == 0) return cudaSuccess;
     e = cudaMemsetAsync(qc, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    k_query_cta<SW, COUNT><<<unsigned(grid), kCtaThreads, smem, st>>>(ix, src, ts, nq, out, sweeps, qc, inv, counters);
+    k_query_cta<COUNT><<<unsigned(grid), kCtaThreads, smem, st>>>(ix, src, ts, nq, out, sweeps, qc, inv, counters);
     return cudaGetLastError();
 }
 
@@ -316,12 +416,21 @@ int cta_grid_size(uint32_t n, int subwarp) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t need = cta_smem_bytes(n) + 64;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k_query_cta<false>) != cudaSuccess) return 0;
+    const size_t need = cta_smem_bytes(n) + fa.sharedSizeBytes;
     if (need > size_t(optin)) return 0;
-    cudaFuncSetAttribute(k_query_cta<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
+    cudaFuncSetAttribute(k_query_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
+    cudaFuncSetAttribute(k_query_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<8, false>, kCtaThreads, cta_smem_bytes(n));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<false>, kCtaThreads, cta_smem_bytes(n));
     return per_sm * sms;
+}
+
+size_t cta_static_smem() {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_query_cta<false>);
+    return fa.sharedSizeBytes;
 }
 
 cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,
@@ -336,22 +445,11 @@ cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_
                              uint64_t nq, uint32_t *d_out, uint32_t *d_sweeps, unsigned long long *d_qcounter,
                              unsigned long long *d_invalid, int grid_cap, unsigned long long *d_counters,
                              cudaStream_t st) {
-#define EAT_CTA_CASE(SWV)                                                                                     \
-    case SWV:                                                                                                 \
-        return d_counters ? launch_cta_sw<SWV, true>(ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter, d_invalid, \
-                                                     grid_cap, d_counters, st)                                \
-                          : launch_cta_sw<SWV, false>(ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter,        \
-                                                      d_invalid, grid_cap, nullptr, st);
-    switch (subwarp) {
-        EAT_CTA_CASE(1)
-        EAT_CTA_CASE(2)
-        EAT_CTA_CASE(4)
-        EAT_CTA_CASE(8)
-        EAT_CTA_CASE(16)
-        EAT_CTA_CASE(32)
-        default: return cudaErrorInvalidValue;
-    }
-#undef EAT_CTA_CASE
+    (void)subwarp;  // the CTA kernel flattens (vertex, type) pairs: no sub-warps
+    return d_counters ? launch_cta_sw<true>(ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter, d_invalid, grid_cap,
+                                            d_counters, st)
+                      : launch_cta_sw<false>(ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter, d_invalid, grid_cap,
+                                             nullptr, st);
 }
 
 cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,

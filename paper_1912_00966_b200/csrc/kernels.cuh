@@ -9,6 +9,7 @@ namespace eat {
 struct DevIndex {
     uint32_t n;                 // |V| (all vertices; a partition owns a sub-range of sources)
     uint32_t cs;                // cluster seconds
+    uint32_t window;            // CTA schedule: process frontier vertices with e[u] <= min + window (kInf = all)
     uint64_t num_types;
     const uint32_t *type_ptr;   // [n+1]
     const uint4 *type_rec;      // [2*T]  (32 B per type)
@@ -49,5 +50,8 @@ cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const 
 
 // Occupancy-derived grid size of the CTA kernel for n vertices (0 if arr does not fit).
 int cta_grid_size(uint32_t n, int subwarp);
+
+// Static shared memory of the CTA kernel (bytes).
+size_t cta_static_smem();
 
 }  // namespace eat

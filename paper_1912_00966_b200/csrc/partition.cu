@@ -225,4 +225,48 @@ eat_status part_query(const DevIndex &ix, PartWork &w, ncclComm_t comm, uint32_t
     return EAT_OK;
 }
 
+eat_status part_query_loopback(const std::vector<DevIndex> &ix, std::vector<PartWork *> &w,
+                               const std::vector<uint32_t> &lo, const std::vector<uint32_t> &hi, int subwarp,
+                               uint32_t s, uint32_t t_s, uint32_t *d_out, cudaStream_t st, uint32_t *rounds,
+                               uint32_t *sweeps, std::string &err) {
+    auto cuda_fail = [&](cudaError_t e, const char *what) {
+        err = std::string(what) + ": " + cudaGetErrorString(e);
+        return EAT_ECUDA;
+    };
+    const size_t P = ix.size();
+    const uint64_t words = uint64_t(ix[0].n) + 1;
+    cudaError_t e;
+    uint32_t r = 0;
+    for (;; ++r) {
+        for (size_t p = 0; p < P; ++p)
+            if ((e = launch_part_round(ix[p], *w[p], lo[p], hi[p], subwarp, r == 0, s, t_s, st)) != cudaSuccess)
+                return cuda_fail(e, "part round");
+        // exchange: min over partitions of e[] ++ flag, then broadcast
+        for (size_t p = 1; p < P; ++p)
+            if ((e = launch_min_merge(w[0]->arr, w[p]->arr, words, st)) != cudaSuccess) return cuda_fail(e, "min merge");
+        for (size_t p = 1; p < P; ++p)
+            if ((e = cudaMemcpyAsync(w[p]->arr, w[0]->arr, words * 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+                return cuda_fail(e, "broadcast");
+        if ((e = cudaMemcpyAsync(w[0]->h_flag, w[0]->arr + ix[0].n, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+            return cuda_fail(e, "flag copy");
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "round sync");
+        if (w[0]->h_flag[0] == 1u) break;
+        if (r > 4u * ix[0].n + 16u) {
+            err = "edge-partitioned query did not converge";
+            return EAT_ECUDA;
+        }
+    }
+    if ((e = launch_gather(ix[0], w[0]->arr, d_out, st)) != cudaSuccess) return cuda_fail(e, "gather");
+    uint32_t total = 0;
+    for (size_t p = 0; p < P; ++p) {
+        if ((e = cudaMemcpyAsync(w[p]->h_flag + 1, w[p]->ctl + 8, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+            return cuda_fail(e, "sweeps copy");
+    }
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "final sync");
+    for (size_t p = 0; p < P; ++p) total = std::max(total, w[p]->h_flag[1]);
+    if (rounds) *rounds = r + 1;
+    if (sweeps) *sweeps = total;
+    return EAT_OK;
+}
+
 }  // namespace eat

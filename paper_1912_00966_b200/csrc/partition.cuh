@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "eat.h"
 #include "kernels.cuh"
@@ -43,5 +44,12 @@ cudaError_t launch_gather(const DevIndex &ix, const uint32_t *arr, uint32_t *out
 eat_status part_query(const DevIndex &ix, PartWork &w, ncclComm_t comm, uint32_t lo, uint32_t hi, int subwarp,
                       uint32_t s, uint32_t t_s, uint32_t *d_out, cudaStream_t st, uint32_t *rounds,
                       uint32_t *sweeps, std::string &err);
+
+// All P partitions on one device (tests / single-GPU runs of the e2 path):
+// the exchange is a device min-merge of the P e[] ++ flag buffers.
+eat_status part_query_loopback(const std::vector<DevIndex> &ix, std::vector<PartWork *> &w,
+                               const std::vector<uint32_t> &lo, const std::vector<uint32_t> &hi, int subwarp,
+                               uint32_t s, uint32_t t_s, uint32_t *d_out, cudaStream_t st, uint32_t *rounds,
+                               uint32_t *sweeps, std::string &err);
 
 }  // namespace eat

@@ -37,7 +37,7 @@ class Engine:
     def __init__(self, num_vertices: int, u, v, dep, dur, xy=None, *, cluster_seconds: int = 3600,
                  renumber: str = "auto", kernel: str = "auto", subwarp: int = 8, device: int = -1,
                  host_only: bool = False, counters: bool = False, mode: str = "replicated", part_rank: int = 0, part_count: int = 1,
-                 nccl_unique_id: Optional[bytes] = None):
+                 nccl_unique_id: Optional[bytes] = None, window: int = 0):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
@@ -55,7 +55,8 @@ class Engine:
                                    flags=(_lib.EAT_BUILD_HOST_ONLY if host_only else 0)
                                    | (_lib.EAT_BUILD_COUNTERS if counters else 0), subwarp=int(subwarp),
                                    mode=_lib.EAT_MODE[mode], part_rank=int(part_rank), part_count=int(part_count),
-                                   nccl_unique_id=ctypes.cast(self._nccl_buf, ctypes.c_void_p) if self._nccl_buf else None)
+                                   nccl_unique_id=ctypes.cast(self._nccl_buf, ctypes.c_void_p) if self._nccl_buf else None,
+                                   window_seconds=int(window))
         self._h = _lib.eat_build(tt, opts)
         self.num_vertices = int(num_vertices)
         self.num_connections = int(m)

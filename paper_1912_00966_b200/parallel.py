@@ -45,13 +45,14 @@ def query_many_sharded(solve: Callable[[np.ndarray, np.ndarray], np.ndarray], so
     all_nv = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(all_nv, t_nv, group=group)
     nv = max(int(x.item()) for x in all_nv)
-    rows = []
-    for r in range(world):
-        a, b = shard_range(src.size, r, world)
-        rows.append(torch.zeros((b - a, nv), dtype=torch.int64))
-    mine = torch.from_numpy(part.astype(np.int64).reshape(hi - lo, nv))
+    # all_gather needs equal shapes: pad every shard to the largest one
+    sizes = [shard_range(src.size, r, world) for r in range(world)]
+    most = max(b - a for a, b in sizes)
+    rows = [torch.zeros((most, nv), dtype=torch.int64) for _ in range(world)]
+    mine = torch.zeros((most, nv), dtype=torch.int64)
+    mine[:hi - lo] = torch.from_numpy(part.astype(np.int64).reshape(hi - lo, nv))
     dist.all_gather(rows, mine, group=group)
-    return torch.cat(rows).numpy().astype(np.uint32)
+    return torch.cat([rows[r][:b - a] for r, (a, b) in enumerate(sizes)]).numpy().astype(np.uint32)
 
 
 def nccl_unique_id(group=None) -> bytes:

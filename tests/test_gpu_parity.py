@@ -209,6 +209,28 @@ def test_metro_single_query():
 
 
 # ----------------------------------------------------------------------------- edge partition
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_edge_partitioned_loopback(P):
+    """e2 on one GPU: P edge partitions (eat_partition_range slices) with the
+    exchange as a device min-merge instead of NCCL -- same local-phase kernel,
+    same round/termination protocol as the multi-GPU path."""
+    for name in ("tiny", "city"):
+        tt = synth.generate(name)
+        eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=P)
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        rng = np.random.default_rng(P)
+        qs = [synth.SINGLE_QUERY] + [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 86400))) for _ in range(4)]
+        for s, t_s in qs:
+            _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"loopback P={P} {name} ({s},{t_s})")
+        assert eng.stats()["last_rounds"] >= 1
+    for seed in range(40):
+        tt = synth.random_small(3000 + seed)
+        eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=P)
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        s, t_s = seed % tt.num_vertices, (seed * 7919) % 86400
+        _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"loopback P={P} seed {seed}")
+
+
 def test_edge_partitioned_single_rank():
     tt = synth.generate("tiny")
     eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=1)
@@ -216,3 +238,21 @@ def test_edge_partitioned_single_rank():
     for s, t_s in [synth.SINGLE_QUERY, (17, 40000)]:
         _assert_rows(eng.query(s, t_s), csa.query(s, t_s), "edge-partitioned P=1")
     assert eng.stats()["last_rounds"] == 1
+
+
+@pytest.mark.parametrize("window", [0, 60, 600, 3600])
+def test_window_schedules_same_fixpoint(window):
+    """The CTA schedule's time window only reorders relaxations (R12): the
+    fixpoint, and so e[], is identical for every window."""
+    tt = synth.generate("tiny")
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    eng = Engine.from_timetable(tt, window=window if window else 0x7FFFFFFF)
+    src, ts = synth.queries(tt, 50, 4)
+    _assert_rows(eng.query_many(src, ts), csa.query_many(src, ts), f"window {window}")
+    for seed in range(60):
+        t2 = synth.random_small(1000 + seed)
+        c2 = oracle.CSA(t2.num_vertices, *t2.arrays())
+        e2 = Engine.from_timetable(t2, window=window if window else 0x7FFFFFFF, kernel="cta")
+        rng = np.random.default_rng(seed)
+        s, t_s = int(rng.integers(t2.num_vertices)), int(rng.integers(0, 86400))
+        _assert_rows(e2.query(s, t_s), c2.query(s, t_s), f"window {window} seed {seed}")
