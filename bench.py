@@ -169,6 +169,116 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+SINGLE_WORKLOADS = {
+    # name: (synth config, engine kwargs, BASELINE configs[] it measures)
+    "city_single": ("city", {}, "BASELINE configs[1]: city, 1 query s=0 t_s=06:00"),
+    "metro_single": ("metro", {}, "BASELINE configs[3]: metro (30% irregular), 1 query s=0 t_s=06:00"),
+    "country_part": ("country", {"mode": "edge_partitioned"},
+                     "BASELINE configs[4]: country, 1 query s=0 t_s=06:00, edge-partitioned over the ranks "
+                     "(NCCL min-allreduce of e[] per exchange round)"),
+}
+
+
+def run_single(args):
+    """Single-query latency workloads (metric: EAT single-query ms)."""
+    import torch
+
+    rank, world, local = _dist()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    import synth
+    from paper_1912_00966_b200 import Engine
+    from paper_1912_00966_b200.parallel import nccl_unique_id
+
+    cfg, kw, desc = SINGLE_WORKLOADS[args.workload]
+    t0 = time.perf_counter()
+    tt = synth.generate(cfg)
+    gen_s = time.perf_counter() - t0
+    kw = dict(kw)
+    if kw.get("mode") == "edge_partitioned":
+        kw.update(part_rank=rank, part_count=world, nccl_unique_id=nccl_unique_id() if world > 1 else None)
+    t0 = time.perf_counter()
+    eng = Engine.from_timetable(tt, device=dev, **kw)
+    build_s = time.perf_counter() - t0
+    st0 = eng.stats()
+    s, t_s = synth.SINGLE_QUERY
+    stream = torch.cuda.Stream(device=dev)
+    out = torch.empty(tt.num_vertices, dtype=torch.int32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
+    for _ in range(args.warmup):
+        eng.query_device(s, t_s, out, stream=stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = Clocks(dev)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k)
+            ev[k][0].record(stream)
+            eng.query_device(s, t_s, out, stream=stream)
+            ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    tot = float(sum(ms))
+    if world > 1:
+        t = torch.tensor([tot], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot = float(t.item())
+    st = eng.stats()
+    # e2e: public host API (D2H of e[] included)
+    h = None
+    t0 = time.perf_counter()
+    reps = max(1, min(args.steps, 5))
+    for _ in range(reps):
+        h = eng.query(s, t_s)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / reps
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        want = csa.query(s, t_s)
+        t0 = time.perf_counter()
+        k = 0
+        while k < 5 and (k == 0 or time.perf_counter() - t0 < args.cpu_seconds):
+            csa.query(s, t_s)
+            k += 1
+        cpu_ms = (time.perf_counter() - t0) * 1e3 / k
+        cpu = {"value": cpu_ms, "unit": "ms", "cores": 1, "kind": "oracle",
+               "sample": f"the same query (s={s}, t_s={t_s}) x{k}, serial CSA (oracle/csa.c), 1 host core",
+               "parity": bool(np.array_equal(h, want))}
+        csa.close()
+    if rank == 0:
+        line = {"metric": "EAT single-query ms", "value": tot / args.steps, "unit": "ms", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps,
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+                "data": "synthetic",
+                "config": {"workload": f"{args.workload} ({desc})", "stops": tt.num_vertices,
+                           "connections": tt.num_connections, "edges": st0["num_edges"], "types": st0["num_types"],
+                           "kernel": st0["kernel_name"], "mode": kw.get("mode", "replicated"),
+                           "l2": "flushed (256 MiB write) between timed steps", "index_bytes": st0["index_bytes"],
+                           "generate_s": gen_s, "build_s": build_s},
+                "sweeps": st["last_sweeps"], "rounds": st["last_rounds"],
+                "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8,
+                        "d2h_bytes_per_step": tt.num_vertices * 4},
+                "gpu_launches": args.steps * max(1, st["last_rounds"]),
+                "clocks": clk, "roofline": None, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def run_gpu(args):
     import torch
 
@@ -328,13 +438,16 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-queries", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="city_batch", choices=["city_batch"] + sorted(SINGLE_WORKLOADS))
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    else:
+    elif args.workload == "city_batch":
         run_gpu(args)
+    else:
+        run_single(args)
 
 
 if __name__ == "__main__":

@@ -104,7 +104,7 @@ typedef struct eat_build_opts {
     int32_t device;               /* CUDA device ordinal; -1 -> current device */
     uint32_t kernel;              /* EAT_KERNEL_* */
     uint32_t flags;               /* EAT_BUILD_* */
-    uint32_t subwarp;             /* lanes per vertex in the relax kernels: 0 -> 8; one of 1,2,4,8,16,32 */
+    uint32_t subwarp;             /* grid kernels: 0 = warp-flattened (vertex,type) pairs (default); 1,2,4,8,16,32 = virtual warps of that width per vertex */
     uint32_t mode;                /* EAT_MODE_* */
     uint32_t part_rank;           /* EDGE_PARTITIONED: this process's rank */
     uint32_t part_count;          /* EDGE_PARTITIONED: number of ranks (1 = single partition) */
@@ -113,6 +113,7 @@ typedef struct eat_build_opts {
                                      e[u] <= min_active(e) + window (others stay active); EAT_INF = every
                                      active vertex (the paper's schedule); 0 -> EAT_DEFAULT_WINDOW.
                                      Results are identical for every value (same fixpoint). */
+    uint32_t cta_threads;         /* CTA kernel threads per query: 0 -> 512; 512, 384 or 256 (occupancy knob) */
 } eat_build_opts;
 
 #define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */

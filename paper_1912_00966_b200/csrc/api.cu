@@ -72,6 +72,7 @@ struct eat_handle {
     uint32_t subwarp = 8;
     uint32_t mode = EAT_MODE_REPLICATED;
     uint32_t window = EAT_INF;           // CTA schedule time window (EAT_INF = all active vertices)
+    uint32_t cta_threads = 512;          // CTA-kernel variant
     cudaStream_t stream = nullptr;
     // device index: slices[0] is this handle's index (whole, or its own edge
     // partition); a loopback edge-partitioned handle holds all P partitions
@@ -165,7 +166,14 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     CUDA_TRY(dalloc_copy(&sl.type_src, tsrc.data(), tsrc.size(), b));
     sl.ix.n = n;
     sl.ix.cs = x.cs;
+    {
+        uint32_t l = 0;
+        while ((1u << l) < x.cs) ++l;  // ceil(log2 cs)
+        sl.ix.cs_shift = 31u + l;
+        sl.ix.cs_magic = uint32_t((1ull << (31u + l)) / x.cs + 1ull);
+    }
     sl.ix.window = h->window;
+    sl.ix.cta_threads = h->cta_threads;
     sl.ix.num_types = T;
     sl.ix.type_ptr = sl.type_ptr;
     sl.ix.type_rec = reinterpret_cast<const uint4 *>(sl.type_rec);
@@ -252,7 +260,7 @@ eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_
 }
 
 eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
-    h->cta_grid = eat::cta_grid_size(h->hx.n, int(h->subwarp));
+    h->cta_grid = eat::cta_grid_size(h->hx.n, int(h->ix.cta_threads));
     h->st.smem_vertices_max = 0;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
@@ -309,9 +317,9 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     eat::BuildParams p;
     p.cs = o.cluster_seconds ? o.cluster_seconds : 3600;
     p.renumber = o.renumber;
-    const uint32_t sw = o.subwarp ? o.subwarp : 8;
-    if (sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
-        return fail(EAT_EINVAL, "subwarp must be 1, 2, 4, 8, 16 or 32");
+    const uint32_t sw = o.subwarp;  // 0: warp-flattened pairs (default)
+    if (sw != 0 && sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
+        return fail(EAT_EINVAL, "subwarp must be 0, 1, 2, 4, 8, 16 or 32");
     if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
     if (o.kernel > EAT_KERNEL_CTA) return fail(EAT_EINVAL, "unknown kernel");
     uint32_t pc = o.part_count ? o.part_count : 1;
@@ -322,6 +330,11 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     h->subwarp = sw;
     h->mode = o.mode;
     h->window = o.window_seconds == 0 ? EAT_DEFAULT_WINDOW : o.window_seconds;
+    h->cta_threads = o.cta_threads == 0 ? 512u : o.cta_threads;
+    if (h->cta_threads != 512 && h->cta_threads != 384 && h->cta_threads != 256) {
+        delete h;
+        return fail(EAT_EINVAL, "cta_threads must be 256, 384 or 512");
+    }
     h->part_rank = o.part_rank;
     h->part_count = pc;
     h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 && !o.nccl_unique_id;

@@ -29,13 +29,20 @@ __device__ __forceinline__ uint32_t item_next(uint32_t it, uint32_t x) {
     return off + q * stride;
 }
 
+// Hour cluster of time e (k = e[u]/3600): exact reciprocal
+// multiply, valid for e < 2^31 (every finite time): the product error is
+// below 2^-l <= 1/cs, so the floor is exact.
+__device__ __forceinline__ uint32_t cluster_of(const DevIndex &ix, uint32_t e) {
+    return uint32_t((uint64_t(e) * ix.cs_magic) >> ix.cs_shift);
+}
+
 // Cluster-AP lookup inside the type's cluster k = eu / cs:
 // smallest term >= eu among the cluster's APs, else the first departure of
 // the next non-empty cluster (precomputed as next_min).
 // Precondition: first < eu <= last (so c_first <= k <= c_last).
 __device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t crec_base, uint32_t c_first,
                                                    uint32_t eu) {
-    const uint32_t k = eu / ix.cs;
+    const uint32_t k = cluster_of(ix, eu);
     const uint32_t r = crec_base + (k - c_first);
     const uint4 r0 = __ldg(ix.crec + 2ull * r);
     const uint32_t x = eu - k * ix.cs;

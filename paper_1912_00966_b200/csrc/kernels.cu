@@ -52,21 +52,22 @@ __global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *boun
 //      a time (owner lane found by a 5-step shuffle search) -- all lanes busy,
 //      no per-vertex divergence, no block scan;
 //   3. next frontier = improved (nxt) + deferred (cur).
-constexpr int kCtaThreads = 512;
-constexpr int kCtaWarps = kCtaThreads / 32;
-constexpr uint32_t kListCap = 2048;  // selected vertices per sweep (overflow stays active)
+// THREADS per CTA and LISTCAP (selected vertices per sweep; overflow stays
+// active) are template parameters: 512/2048 fits 4 CTAs (queries) per SM for
+// a 10k-stop city, 384/512 fits 5.
 
 // COUNT: instrumented variant (EAT_BUILD_COUNTERS) accumulating, per launch,
 // the work counters used for algorithmic-byte accounting:
 // counters[0] vertex visits, [1] type records read, [2] cluster records read,
 // [3] spilled items read, [4] improvements (successful atomicMin), [5] sweeps.
-template <bool COUNT>
-__global__ void __launch_bounds__(kCtaThreads, 4) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
+template <bool COUNT, int kCtaThreads, int kListCap>
+__global__ void __launch_bounds__(kCtaThreads, 2048 / kCtaThreads) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
                                                                const uint32_t *__restrict__ tsv, uint64_t nq,
                                                                uint32_t *__restrict__ out, uint32_t *sweeps_out,
                                                                unsigned long long *qcounter,
                                                                unsigned long long *invalid,
                                                                unsigned long long *counters) {
+    constexpr uint32_t kCtaWarps = kCtaThreads / 32;
     extern __shared__ uint32_t sm[];
     const uint32_t n = ix.n;
     const uint32_t W = (n + 31u) / 32u;
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_query_cta(DevIndex ix, const
                 const uint32_t k = __popc(sel);
                 if (!k) continue;
                 const uint32_t pos = atomicAdd(&s_cnt, k);
-                uint32_t put = pos < kListCap ? min(k, kListCap - pos) : 0u;
+                uint32_t put = pos < uint32_t(kListCap) ? min(k, uint32_t(kListCap) - pos) : 0u;
                 uint32_t taken = 0, rest = sel;
                 for (uint32_t i = 0; i < put; ++i) {
                     const uint32_t b = __ffs(rest) - 1u;
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_query_cta(DevIndex ix, const
             dmin = __reduce_min_sync(0xFFFFFFFFu, dmin);
             if (lane == 0 && dmin < kInf) atomicMin(&s_tmin[nb], dmin);
             __syncthreads();
-            const uint32_t F = min(s_cnt, kListCap);
+            const uint32_t F = min(s_cnt, uint32_t(kListCap));
             // ---- 2. warp-level flattened (vertex, type) pairs; a warp takes g
             // consecutive list entries so that small frontiers still spread
             // over all warps
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_query_cta(DevIndex ix, const
                         tc = cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
                         if (COUNT) {
                             ++c_crec;
-                            const uint4 rr = __ldg(ix.crec + 2ull * (tr.crec_base + eu / ix.cs - tr.c_first));
+                            const uint4 rr = __ldg(ix.crec + 2ull * (tr.crec_base + cluster_of(ix, eu) - tr.c_first));
                             if (rr.y == kItemSpill) c_spill += rr.w;
                         }
                     }
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     // Initialize (Algorithm 2)
     for (uint64_t i = gtid; i < n; i += gsz) {
         w.arr[i] = kInf;
-        if (SCHED == kSchedFrontier) w.stamp[i] = 0;
+        if (SCHED != kSchedFull) w.stamp[i] = 0;
     }
     if (SCHED == kSchedFull)
         for (uint64_t i = gtid; i < 3ull * W; i += gsz) w.bm[i] = 0;
@@ -291,12 +292,15 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
         w.ctl[0] = 1;  // sweep 0 sees one active vertex
         w.ctl[1] = 0;
         w.ctl[2] = 0;
+        w.ctl[11] = ts;  // window base (min e[] over the frontier), 3 rotating slots
+        w.ctl[12] = kInf;
+        w.ctl[13] = kInf;
     }
     grid_sync(bar);
     if (gtid == 0) {
         const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
         w.arr[si] = ts;
-        if (SCHED == kSchedFrontier) w.q0[0] = si;
+        if (SCHED != kSchedFull) w.q0[0] = si;
         else w.bm[si >> 5] = 1u << (si & 31u);
     }
     grid_sync(bar);
@@ -305,7 +309,74 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     for (;;) {
         const uint32_t c_cur = sweep % 3u, c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
         if (gtid == 0) w.ctl[c_old] = 0;
-        if (SCHED == kSchedFrontier) {
+        if (SCHED == kSchedFlat) {
+            // worklist + time window + warp-flattened (vertex, type) pairs
+            const uint32_t cnt = ld_cg(w.ctl + c_cur);
+            const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
+            uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
+            const uint32_t t_cur = sweep % 3u, t_nxt = (sweep + 1u) % 3u, t_old = (sweep + 2u) % 3u;
+            if (gtid == 0) w.ctl[11 + t_old] = kInf;
+            uint32_t thr = kInf;
+            if (ix.window < kInf) {
+                const uint32_t base = ld_cg(w.ctl + 11 + t_cur);
+                thr = base + min(ix.window, kInf - base);
+            }
+            const uint32_t lane = threadIdx.x & 31u;
+            const uint64_t wid = gtid >> 5, nwarps = gsz >> 5;
+            uint64_t gg = (cnt + nwarps - 1) / nwarps;
+            const uint32_t g = uint32_t(gg < 1 ? 1 : (gg > 32 ? 32 : gg));
+            for (uint64_t k0 = wid * g; k0 < cnt; k0 += nwarps * g) {
+                uint32_t x = 0, p0 = 0, nt = 0;
+                if (lane < g && k0 + lane < cnt) {
+                    x = ld_cg(qc + k0 + lane);
+                    const uint32_t ex = ld_cg(w.arr + x);
+                    if (ex <= thr) {
+                        p0 = __ldg(ix.type_ptr + x);
+                        nt = __ldg(ix.type_ptr + x + 1) - p0;
+                    } else {  // deferred: stays on the frontier
+                        atomicMin(w.ctl + 11 + t_nxt, ex);
+                        if (atomicExch(w.stamp + x, sweep + 1u) != sweep + 1u) push_aggregated(x, qn, w.ctl + c_nxt);
+                    }
+                }
+                uint32_t incl = nt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= uint32_t(o)) incl += y;
+                }
+                const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                for (uint32_t base = 0; base < tot; base += 32u) {
+                    const uint32_t qp = base + lane;
+                    uint32_t L = 0;
+#pragma unroll
+                    for (uint32_t step = 16; step > 0; step >>= 1) {
+                        const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, L + step - 1u);
+                        if (v <= qp) L += step;
+                    }
+                    const uint32_t o_incl = __shfl_sync(0xFFFFFFFFu, incl, L);
+                    const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
+                    const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
+                    const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
+                    if (qp >= tot) continue;
+                    const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
+                    const uint32_t eu = ld_cg(w.arr + u);
+                    const TypeRec tr = load_type(ix, t);
+                    if (eu > tr.last) continue;
+                    const uint32_t av = ld_cg(w.arr + tr.v);
+                    if (max(eu, tr.first) + tr.lam >= av) continue;
+                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                    const uint32_t cand = tc + tr.lam;
+                    if (cand < av) {
+                        const uint32_t old = atomicMin(w.arr + tr.v, cand);
+                        if (cand < old) {
+                            if (ix.window < kInf) atomicMin(w.ctl + 11 + t_nxt, cand);
+                            if (atomicExch(w.stamp + tr.v, sweep + 1u) != sweep + 1u)
+                                push_aggregated(tr.v, qn, w.ctl + c_nxt);
+                        }
+                    }
+                }
+            }
+        } else if (SCHED == kSchedFrontier) {
             const uint32_t cnt = ld_cg(w.ctl + c_cur);
             const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
             uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
@@ -362,17 +433,17 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     if (gtid == 0) w.ctl[8] = sweep;
 }
 
-template <bool COUNT>
+template <bool COUNT, int T, int L>
 cudaError_t launch_cta_sw(const DevIndex &ix, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
                           uint32_t *sweeps, unsigned long long *qc, unsigned long long *inv, int grid_cap,
                           unsigned long long *counters, cudaStream_t st) {
     const size_t smem = cta_smem_bytes(ix.n);
-    cudaError_t e = cudaFuncSetAttribute(k_query_cta<COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = cudaFuncSetAttribute(k_query_cta<COUNT, T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<COUNT>, kCtaThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<COUNT, T, L>, T, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = std::min<uint64_t>(uint64_t(sms) * per_sm, nq);
@@ -380,8 +451,19 @@ cudaError_t launch_cta_sw(const DevIndex &ix, const uint32_t *src, const uint32_
     if (grid == 0) return cudaSuccess;
     e = cudaMemsetAsync(qc, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    k_query_cta<COUNT><<<unsigned(grid), kCtaThreads, smem, st>>>(ix, src, ts, nq, out, sweeps, qc, inv, counters);
+    k_query_cta<COUNT, T, L><<<unsigned(grid), T, smem, st>>>(ix, src, ts, nq, out, sweeps, qc, inv, counters);
     return cudaGetLastError();
+}
+
+template <bool COUNT>
+cudaError_t launch_cta_variant(int variant, const DevIndex &ix, const uint32_t *src, const uint32_t *ts, uint64_t nq,
+                               uint32_t *out, uint32_t *sweeps, unsigned long long *qc, unsigned long long *inv,
+                               int grid_cap, unsigned long long *counters, cudaStream_t st) {
+    switch (variant) {
+        case 384: return launch_cta_sw<COUNT, 384, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
+        case 256: return launch_cta_sw<COUNT, 256, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
+        default: return launch_cta_sw<COUNT, 512, 2048>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
+    }
 }
 
 template <int SW, int SCHED>
@@ -410,26 +492,34 @@ size_t cta_smem_bytes(uint32_t n) {
     return (npad + 2 * W) * sizeof(uint32_t);
 }
 
-int cta_grid_size(uint32_t n, int subwarp) {
-    (void)subwarp;
+template <int T, int L>
+int cta_grid_size_t(uint32_t n) {
     int dev = 0, optin = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, k_query_cta<false>) != cudaSuccess) return 0;
+    if (cudaFuncGetAttributes(&fa, k_query_cta<false, T, L>) != cudaSuccess) return 0;
     const size_t need = cta_smem_bytes(n) + fa.sharedSizeBytes;
     if (need > size_t(optin)) return 0;
-    cudaFuncSetAttribute(k_query_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
-    cudaFuncSetAttribute(k_query_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
+    cudaFuncSetAttribute(k_query_cta<false, T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
+    cudaFuncSetAttribute(k_query_cta<true, T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<false>, kCtaThreads, cta_smem_bytes(n));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<false, T, L>, T, cta_smem_bytes(n));
     return per_sm * sms;
+}
+
+int cta_grid_size(uint32_t n, int variant) {
+    switch (variant) {
+        case 384: return cta_grid_size_t<384, 512>(n);
+        case 256: return cta_grid_size_t<256, 512>(n);
+        default: return cta_grid_size_t<512, 2048>(n);
+    }
 }
 
 size_t cta_static_smem() {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_query_cta<false>);
+    cudaFuncGetAttributes(&fa, k_query_cta<false, 512, 2048>);
     return fa.sharedSizeBytes;
 }
 
@@ -446,15 +536,16 @@ cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_
                              unsigned long long *d_invalid, int grid_cap, unsigned long long *d_counters,
                              cudaStream_t st) {
     (void)subwarp;  // the CTA kernel flattens (vertex, type) pairs: no sub-warps
-    return d_counters ? launch_cta_sw<true>(ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter, d_invalid, grid_cap,
-                                            d_counters, st)
-                      : launch_cta_sw<false>(ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter, d_invalid, grid_cap,
-                                             nullptr, st);
+    return d_counters ? launch_cta_variant<true>(ix.cta_threads, ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter,
+                                                 d_invalid, grid_cap, d_counters, st)
+                      : launch_cta_variant<false>(ix.cta_threads, ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter,
+                                                  d_invalid, grid_cap, nullptr, st);
 }
 
 cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,
                               uint32_t t_s, uint32_t *d_out, cudaStream_t st) {
     if (sched == kSchedFull) return launch_grid_sw<1, kSchedFull>(ix, w, s, t_s, d_out, st);
+    if (subwarp == 0) return launch_grid_sw<32, kSchedFlat>(ix, w, s, t_s, d_out, st);
     switch (subwarp) {
         case 1: return launch_grid_sw<1, kSchedFrontier>(ix, w, s, t_s, d_out, st);
         case 2: return launch_grid_sw<2, kSchedFrontier>(ix, w, s, t_s, d_out, st);

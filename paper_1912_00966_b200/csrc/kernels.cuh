@@ -10,6 +10,9 @@ struct DevIndex {
     uint32_t n;                 // |V| (all vertices; a partition owns a sub-range of sources)
     uint32_t cs;                // cluster seconds
     uint32_t window;            // CTA schedule: process frontier vertices with e[u] <= min + window (kInf = all)
+    uint32_t cta_threads;       // CTA-kernel variant: 512 (default), 384 or 256 threads per query
+    uint32_t cs_magic;          // floor(2^(31+l) / cs) + 1, l = ceil(log2 cs): e / cs == (e * cs_magic) >> (31 + l)
+    uint32_t cs_shift;          // 31 + l   (exact for every e < 2^31)
     uint64_t num_types;
     const uint32_t *type_ptr;   // [n+1]
     const uint4 *type_rec;      // [2*T]  (32 B per type)
@@ -25,10 +28,10 @@ struct GridWork {
     uint32_t *q0, *q1;   // [n] frontier worklists (ping-pong)
     uint32_t *stamp;     // [n] "queued for sweep k" stamps (dedup)
     uint32_t *bm;        // [3*W] rotating active bitmaps (full-sweep schedule)
-    uint32_t *ctl;       // [16] control words: 0-2 rotating counters, 4-5 grid barrier, 8 sweeps
+    uint32_t *ctl;       // [16] control words: 0-2 rotating counters, 4-5 grid barrier, 8 sweeps, 11-13 window base
 };
 
-enum { kSchedFrontier = 0, kSchedFull = 1 };
+enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2 };
 
 // Largest dynamic shared memory (bytes) the CTA kernel may use on `device`.
 size_t cta_smem_bytes(uint32_t n);
@@ -45,11 +48,12 @@ cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_
                              cudaStream_t st);
 
 // Grid-wide persistent kernel for one query with global arr (cooperative launch).
+// subwarp 0: warp-flattened pairs + time window (default); 1..32: virtual warps of that width.
 cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,
                               uint32_t t_s, uint32_t *d_out, cudaStream_t st);
 
-// Occupancy-derived grid size of the CTA kernel for n vertices (0 if arr does not fit).
-int cta_grid_size(uint32_t n, int subwarp);
+// Occupancy-derived grid size of the CTA kernel variant for n vertices (0 if arr does not fit).
+int cta_grid_size(uint32_t n, int variant);
 
 // Static shared memory of the CTA kernel (bytes).
 size_t cta_static_smem();

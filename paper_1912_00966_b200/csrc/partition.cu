@@ -166,6 +166,7 @@ cudaError_t launch_part_round(const DevIndex &ix, const PartWork &w, uint32_t lo
     cudaError_t e = cudaMemsetAsync(w.ctl + 4, 0, 2 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     switch (subwarp) {
+        case 0: return launch_round_sw<8>(ix, w, lo, hi, first, s, t_s, st);
         case 1: return launch_round_sw<1>(ix, w, lo, hi, first, s, t_s, st);
         case 2: return launch_round_sw<2>(ix, w, lo, hi, first, s, t_s, st);
         case 4: return launch_round_sw<4>(ix, w, lo, hi, first, s, t_s, st);

@@ -35,9 +35,10 @@ class Engine:
     """A built EAT index on one device (or one edge partition of it)."""
 
     def __init__(self, num_vertices: int, u, v, dep, dur, xy=None, *, cluster_seconds: int = 3600,
-                 renumber: str = "auto", kernel: str = "auto", subwarp: int = 8, device: int = -1,
+                 renumber: str = "auto", kernel: str = "auto", subwarp: int = 0, device: int = -1,
                  host_only: bool = False, counters: bool = False, mode: str = "replicated", part_rank: int = 0, part_count: int = 1,
-                 nccl_unique_id: Optional[bytes] = None, window: int = 0):
+                 nccl_unique_id: Optional[bytes] = None, window: int = 0,
+                 cta_threads: int = 0):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
@@ -56,7 +57,7 @@ class Engine:
                                    | (_lib.EAT_BUILD_COUNTERS if counters else 0), subwarp=int(subwarp),
                                    mode=_lib.EAT_MODE[mode], part_rank=int(part_rank), part_count=int(part_count),
                                    nccl_unique_id=ctypes.cast(self._nccl_buf, ctypes.c_void_p) if self._nccl_buf else None,
-                                   window_seconds=int(window))
+                                   window_seconds=int(window), cta_threads=int(cta_threads))
         self._h = _lib.eat_build(tt, opts)
         self.num_vertices = int(num_vertices)
         self.num_connections = int(m)

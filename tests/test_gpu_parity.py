@@ -256,3 +256,16 @@ def test_window_schedules_same_fixpoint(window):
         rng = np.random.default_rng(seed)
         s, t_s = int(rng.integers(t2.num_vertices)), int(rng.integers(0, 86400))
         _assert_rows(e2.query(s, t_s), c2.query(s, t_s), f"window {window} seed {seed}")
+
+
+@pytest.mark.skipif(not __import__("os").environ.get("EAT_TEST_COUNTRY"), reason="set EAT_TEST_COUNTRY=1 (minutes)")
+def test_country_single_query():
+    """BASELINE configs[4] at N=1: country (1M stops, ~300M connections),
+    edge-partitioned code path (P=1 and loopback P=2), vs the oracle."""
+    tt = synth.generate("country")
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    want = csa.query(*synth.SINGLE_QUERY)
+    for kw in ({}, {"mode": "edge_partitioned", "part_count": 1}, {"mode": "edge_partitioned", "part_count": 2}):
+        eng = Engine.from_timetable(tt, **kw)
+        _assert_rows(eng.query(*synth.SINGLE_QUERY), want, f"country {kw}")
+        eng.close()
