@@ -82,10 +82,14 @@ enum {
 
 /* eat_build_opts.kernel: relaxation schedule for single queries. */
 enum {
-    EAT_KERNEL_AUTO = 0,          /* CTA kernel when arr fits shared memory, else FRONTIER */
+    EAT_KERNEL_AUTO = 0,          /* CTA kernel when arr fits shared memory, else ASYNC when a 1/148
+                                     slice fits, else FRONTIER */
     EAT_KERNEL_FRONTIER = 1,      /* grid-wide persistent kernel, worklist frontier, global arr */
     EAT_KERNEL_FULL_SWEEP = 2,    /* grid-wide persistent kernel, every type every sweep, active bitmap */
-    EAT_KERNEL_CTA = 3            /* one CTA per query, arr in shared memory */
+    EAT_KERNEL_CTA = 3,           /* one CTA per query, arr in shared memory */
+    EAT_KERNEL_ASYNC = 4          /* CTA-partitioned: each CTA owns a vertex range (e[] slice in shared
+                                     memory), sweeps locally to quiescence, exchanges via global atomicMin
+                                     + inboxes; one grid barrier per exchange round */
 };
 
 /* eat_build_opts.mode */
@@ -104,16 +108,19 @@ typedef struct eat_build_opts {
     int32_t device;               /* CUDA device ordinal; -1 -> current device */
     uint32_t kernel;              /* EAT_KERNEL_* */
     uint32_t flags;               /* EAT_BUILD_* */
-    uint32_t subwarp;             /* grid kernels: 0 = warp-flattened (vertex,type) pairs (default); 1,2,4,8,16,32 = virtual warps of that width per vertex */
+    uint32_t subwarp;             /* grid kernels (FRONTIER, edge partition): lanes per active vertex, 1,2,4,8,16,32
+                                     (virtual warps; 0 -> 32 = the Warps-version);
+                                     64 = warp-flattened (vertex, type) pairs with the time window */
     uint32_t mode;                /* EAT_MODE_* */
     uint32_t part_rank;           /* EDGE_PARTITIONED: this process's rank */
     uint32_t part_count;          /* EDGE_PARTITIONED: number of ranks (1 = single partition) */
     const void *nccl_unique_id;   /* EDGE_PARTITIONED with part_count > 1: 128-byte ncclUniqueId, same on every rank */
-    uint32_t window_seconds;      /* CTA-kernel schedule: a sweep relaxes the active vertices with
+    uint32_t window_seconds;      /* CTA-kernel schedule (and grid kernel with subwarp 64): a sweep relaxes the active vertices with
                                      e[u] <= min_active(e) + window (others stay active); EAT_INF = every
                                      active vertex (the paper's schedule); 0 -> EAT_DEFAULT_WINDOW.
                                      Results are identical for every value (same fixpoint). */
-    uint32_t cta_threads;         /* CTA kernel threads per query: 0 -> 512; 512, 384 or 256 (occupancy knob) */
+    uint32_t cta_threads;         /* CTA kernel threads per query: 0 -> 256; 512, 384 or 256 (occupancy knob,
+                                     tools/sweep_cta.py) */
 } eat_build_opts;
 
 #define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */

@@ -16,6 +16,7 @@
 #include "eat.h"
 #include "eat_internal.h"
 #include "kernels.cuh"
+#include "async.cuh"
 #include "partition.cuh"
 
 namespace {
@@ -83,9 +84,11 @@ struct eat_handle {
     bool loopback = false;
     // single-query scratch
     eat::GridWork gw{};
+    eat::AsyncWork aw{};
     uint32_t *d_out1 = nullptr, *h_out1 = nullptr;
     uint32_t *d_q1 = nullptr;  // [2]: s, t_s for the CTA kernel
     uint32_t *d_sweeps1 = nullptr;
+    uint32_t *d_rounds1 = nullptr;   // async kernel: exchange rounds of the last query
     unsigned long long *d_counter = nullptr, *d_invalid = nullptr;
     unsigned long long *d_work = nullptr;  // EAT_BUILD_COUNTERS: 6 work counters
     // batched scratch
@@ -106,9 +109,10 @@ void release_device(eat_handle *h) {
     cudaSetDevice(h->device);
     void *ptrs[] = {h->d_perm,  h->gw.arr, h->gw.q0,     h->gw.q1,      h->gw.stamp,   h->gw.bm,
                     h->gw.ctl,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
-                    h->d_bsrc,  h->d_bts,  h->d_bout,    h->d_work};
+                    h->d_bsrc,  h->d_bts,  h->d_bout,    h->d_work, h->d_rounds1};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    eat::async_free(h->aw);
     for (Slice &sl : h->slices) {
         void *sp[] = {sl.type_ptr, sl.type_rec, sl.crec, sl.pool, sl.type_src};
         for (void *p : sp)
@@ -221,6 +225,8 @@ eat_status upload(eat_handle *h) {
     CUDA_TRY(cudaMalloc(&h->d_q1, 2 * 4));
     CUDA_TRY(cudaMalloc(&h->d_sweeps1, 4));
     CUDA_TRY(cudaMemset(h->d_sweeps1, 0, 4));
+    CUDA_TRY(cudaMalloc(&h->d_rounds1, 4));
+    CUDA_TRY(cudaMemset(h->d_rounds1, 0, 4));
     CUDA_TRY(cudaMalloc(&h->d_counter, 8));
     CUDA_TRY(cudaMalloc(&h->d_invalid, 8));
     CUDA_TRY(cudaMemset(h->d_invalid, 0, 8));
@@ -268,10 +274,19 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     const size_t avail = size_t(optin) - eat::cta_static_smem() - 64;
     h->st.smem_vertices_max = uint32_t(avail * 32 / (4 * 32 + 2 * 4));
     uint32_t k = requested;
-    if (k == EAT_KERNEL_AUTO) k = h->cta_grid > 0 ? EAT_KERNEL_CTA : EAT_KERNEL_FRONTIER;
+    const bool async_ok = eat::async_parts(h->hx.n) > 0;
+    if (k == EAT_KERNEL_AUTO) k = h->cta_grid > 0 ? EAT_KERNEL_CTA : (async_ok ? EAT_KERNEL_ASYNC : EAT_KERNEL_FRONTIER);
     if (k == EAT_KERNEL_CTA && h->cta_grid == 0)
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
-    if (k > EAT_KERNEL_CTA) return fail(EAT_EINVAL, "unknown kernel");
+    if (k == EAT_KERNEL_ASYNC && !async_ok)
+        return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_ASYNC: a 1/SM-count slice of the arrival array does not fit shared memory");
+    if (k > EAT_KERNEL_ASYNC) return fail(EAT_EINVAL, "unknown kernel");
+    if (k == EAT_KERNEL_ASYNC) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (eat::async_alloc(h->aw, h->hx.n, uint32_t(sms)) != cudaSuccess)
+            return fail(EAT_ENOMEM, "cannot allocate async-kernel scratch");
+    }
     h->kernel = k;
     h->st.kernel = k;
     return EAT_OK;
@@ -294,6 +309,10 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
         CUDA_TRY(cudaMemcpyAsync(h->d_q1, q, sizeof(q), cudaMemcpyHostToDevice, st));
         CUDA_TRY(eat::launch_query_cta(h->ix, int(h->subwarp), h->d_q1, h->d_q1 + 1, 1, d_out, h->d_sweeps1,
                                        h->d_counter, h->d_invalid, 1, nullptr, st));
+    } else if (h->kernel == EAT_KERNEL_ASYNC) {
+        CUDA_TRY(eat::launch_query_async(h->ix, h->aw, s, t_s, d_out, st));
+        CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->aw.ctl + 9, 4, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(h->d_rounds1, h->aw.ctl + 8, 4, cudaMemcpyDeviceToDevice, st));
     } else {
         int sched = h->kernel == EAT_KERNEL_FULL_SWEEP ? eat::kSchedFull : eat::kSchedFrontier;
         CUDA_TRY(eat::launch_query_grid(h->ix, int(h->subwarp), sched, h->gw, s, t_s, d_out, st));
@@ -317,11 +336,11 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     eat::BuildParams p;
     p.cs = o.cluster_seconds ? o.cluster_seconds : 3600;
     p.renumber = o.renumber;
-    const uint32_t sw = o.subwarp;  // 0: warp-flattened pairs (default)
+    const uint32_t sw = o.subwarp == 0 ? 32u : (o.subwarp == 64 ? 0u : o.subwarp);  // 0 internally = flattened
     if (sw != 0 && sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
-        return fail(EAT_EINVAL, "subwarp must be 0, 1, 2, 4, 8, 16 or 32");
+        return fail(EAT_EINVAL, "subwarp must be 0 (default 32), 1, 2, 4, 8, 16, 32 or 64 (flattened pairs)");
     if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
-    if (o.kernel > EAT_KERNEL_CTA) return fail(EAT_EINVAL, "unknown kernel");
+    if (o.kernel > EAT_KERNEL_ASYNC) return fail(EAT_EINVAL, "unknown kernel");
     uint32_t pc = o.part_count ? o.part_count : 1;
     if (o.mode == EAT_MODE_EDGE_PARTITIONED && o.part_rank >= pc)
         return fail(EAT_EINVAL, "edge partition needs part_rank < part_count");
@@ -330,7 +349,7 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     h->subwarp = sw;
     h->mode = o.mode;
     h->window = o.window_seconds == 0 ? EAT_DEFAULT_WINDOW : o.window_seconds;
-    h->cta_threads = o.cta_threads == 0 ? 512u : o.cta_threads;
+    h->cta_threads = o.cta_threads == 0 ? 256u : o.cta_threads;
     if (h->cta_threads != 512 && h->cta_threads != 384 && h->cta_threads != 256) {
         delete h;
         return fail(EAT_EINVAL, "cta_threads must be 256, 384 or 512");
@@ -438,6 +457,11 @@ eat_status eat_get_stats(const eat_handle *hc, eat_stats *out) {
         CUDA_TRY(cudaMemcpy(&inv, h->d_invalid, 8, cudaMemcpyDeviceToHost));
         h->st.last_sweeps = sw;
         h->st.invalid_queries = inv;
+        if (h->kernel == EAT_KERNEL_ASYNC && h->mode != EAT_MODE_EDGE_PARTITIONED) {
+            uint32_t rr = 0;
+            CUDA_TRY(cudaMemcpy(&rr, h->d_rounds1, 4, cudaMemcpyDeviceToHost));
+            h->st.last_rounds = rr;
+        }
         if (h->d_work) {
             unsigned long long w[6];
             CUDA_TRY(cudaMemcpy(w, h->d_work, sizeof(w), cudaMemcpyDeviceToHost));
@@ -513,8 +537,8 @@ eat_status eat_query_many_device(eat_handle *h, const uint32_t *d_sources, const
             CUDA_TRY(cudaStreamSynchronize(st));
             continue;
         }
-        int sched = h->kernel == EAT_KERNEL_FULL_SWEEP ? eat::kSchedFull : eat::kSchedFrontier;
-        CUDA_TRY(eat::launch_query_grid(h->ix, int(h->subwarp), sched, h->gw, hs[q], ht[q], row, st));
+        eat_status e = enqueue_single(h, hs[q], ht[q], row, st);
+        if (e != EAT_OK) return e;
     }
     return EAT_OK;
 }

@@ -25,8 +25,14 @@ __device__ __forceinline__ uint32_t item_next(uint32_t it, uint32_t x) {
     if (x <= off) return off;
     const uint32_t last = off + cm1 * stride;
     if (x > last) return kNone;  // also covers singletons (cm1 == 0): stride unused
-    const uint32_t q = (x - off + stride - 1u) / stride;
-    return off + q * stride;
+    // ceil((x - off) / stride) for 12-bit operands: float estimate of the
+    // floor (error < 1), then an exact integer fix-up
+    const uint32_t a = x - off;
+    uint32_t q = __float2uint_rz(__fdividef(__uint2float_rz(a), __uint2float_rz(stride)));  // MUFU.RCP-based
+    int32_t r = int32_t(a) - int32_t(q * stride);
+    if (r < 0) { --q; r += int32_t(stride); }
+    if (r >= int32_t(stride)) { ++q; r -= int32_t(stride); }
+    return off + (q + (r != 0 ? 1u : 0u)) * stride;
 }
 
 // Hour cluster of time e (k = e[u]/3600): exact reciprocal

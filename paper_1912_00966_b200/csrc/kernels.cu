@@ -13,6 +13,7 @@
 //     (PAPER.md:403-409); a strict improvement marks v in the NEXT frontier.
 // Sweeps repeat until the next frontier is empty.
 #include <algorithm>
+#include <cstdlib>
 #include <cuda/atomic>
 #include <cuda_runtime.h>
 
@@ -25,6 +26,21 @@ namespace eat {
 namespace {
 
 using namespace dev;
+
+}  // namespace
+
+// CTAs per SM of the persistent grid kernels (fewer CTAs = cheaper grid
+// barrier): EAT_GRID_CTAS_PER_SM (1..8, default 4; tuning knob).
+int grid_ctas_per_sm() {
+    static int v = [] {
+        const char *e = getenv("EAT_GRID_CTAS_PER_SM");
+        int x = e ? atoi(e) : 4;
+        return x < 1 ? 1 : (x > 8 ? 8 : x);
+    }();
+    return v;
+}
+
+namespace {
 
 // ---------------------------------------------------------------- lookup kernel
 __global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *bound, uint64_t n, uint32_t *out) {
@@ -60,8 +76,13 @@ __global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *boun
 // the work counters used for algorithmic-byte accounting:
 // counters[0] vertex visits, [1] type records read, [2] cluster records read,
 // [3] spilled items read, [4] improvements (successful atomicMin), [5] sweeps.
+// Minimum resident CTAs per SM for the register budget: shared memory (e[]
+// of a 10k-stop city) already caps residency at 4 (512 threads) or 5.
+template <int T>
+constexpr int cta_min_blocks() { return T >= 512 ? 4 : 5; }
+
 template <bool COUNT, int kCtaThreads, int kListCap>
-__global__ void __launch_bounds__(kCtaThreads, 2048 / kCtaThreads) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
+__global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
                                                                const uint32_t *__restrict__ tsv, uint64_t nq,
                                                                uint32_t *__restrict__ out, uint32_t *sweeps_out,
                                                                unsigned long long *qcounter,
@@ -74,11 +95,11 @@ __global__ void __launch_bounds__(kCtaThreads, 2048 / kCtaThreads) k_query_cta(D
     const uint32_t npad = (n + 3u) & ~3u;
     uint32_t *arr = sm;
     volatile uint32_t *varr = sm;
-    uint32_t *bmA = sm + npad;
-    uint32_t *bmB = bmA + W;
+    uint32_t *bmD = sm + npad;  // deferred: active, not yet selected
+    uint32_t *bmN = bmD + W;    // new: lowered since their last selection
     __shared__ uint32_t s_list[kListCap];
-    __shared__ uint32_t s_cnt;
-    __shared__ uint32_t s_tmin[2];
+    __shared__ uint32_t s_cnt[2], s_more[2];  // per sweep parity: listed / (deferred + improved)
+    __shared__ uint32_t s_tmin[3];            // window base, rotating per sweep
     __shared__ unsigned long long s_q;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
     const uint32_t window = ix.window;
@@ -102,36 +123,38 @@ __global__ void __launch_bounds__(kCtaThreads, 2048 / kCtaThreads) k_query_cta(D
         // Initialize (Algorithm 2)
         for (uint32_t i = tid; i < n; i += kCtaThreads) arr[i] = kInf;
         for (uint32_t i = tid; i < W; i += kCtaThreads) {
-            bmA[i] = 0;
-            bmB[i] = 0;
+            bmD[i] = 0;
+            bmN[i] = 0;
         }
         if (tid == 0) {
-            s_cnt = 0;
+            s_cnt[0] = s_cnt[1] = 0;
+            s_more[0] = s_more[1] = 0;
             s_tmin[0] = ts;
-            s_tmin[1] = kInf;
+            s_tmin[1] = s_tmin[2] = kInf;
         }
         __syncthreads();
         if (tid == 0) {
             const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
             arr[si] = ts;
-            bmA[si >> 5] = 1u << (si & 31u);
+            bmN[si >> 5] = 1u << (si & 31u);
         }
         __syncthreads();
-        uint32_t *cur = bmA, *nxt = bmB;
         uint32_t sweeps = 0;
         uint32_t c_vis = 0, c_type = 0, c_crec = 0, c_spill = 0, c_impr = 0;
         for (;;) {
-            const uint32_t nb = (sweeps + 1u) & 1u;  // s_tmin slot written by this sweep
+            const uint32_t p = sweeps & 1u;
+            const uint32_t t_nxt = (sweeps + 1u) % 3u;  // s_tmin slot written by this sweep
             uint32_t thr = kInf;
             if (window < kInf) {
-                const uint32_t base = s_tmin[sweeps & 1u];
+                const uint32_t base = s_tmin[sweeps % 3u];
                 thr = base + min(window, kInf - base);  // saturating
             }
-            // ---- 1. select + compact
-            uint32_t dmin = kInf;
+            // ---- 1. select + compact: active = deferred | new
+            uint32_t dmin = kInf, ndef = 0;
             for (uint32_t w = tid; w < W; w += kCtaThreads) {
-                const uint32_t word = cur[w];
+                const uint32_t word = bmD[w] | bmN[w];
                 if (!word) continue;
+                bmN[w] = 0;
                 uint32_t sel = word;
                 if (thr < kInf) {
                     sel = 0;
@@ -144,32 +167,45 @@ __global__ void __launch_bounds__(kCtaThreads, 2048 / kCtaThreads) k_query_cta(D
                         else dmin = min(dmin, a);
                     }
                 }
+                uint32_t taken = 0;
                 const uint32_t k = __popc(sel);
-                if (!k) continue;
-                const uint32_t pos = atomicAdd(&s_cnt, k);
-                uint32_t put = pos < uint32_t(kListCap) ? min(k, uint32_t(kListCap) - pos) : 0u;
-                uint32_t taken = 0, rest = sel;
-                for (uint32_t i = 0; i < put; ++i) {
-                    const uint32_t b = __ffs(rest) - 1u;
-                    rest &= rest - 1u;
-                    s_list[pos + i] = w * 32u + b;
-                    taken |= 1u << b;
+                if (k) {
+                    const uint32_t pos = atomicAdd(&s_cnt[p], k);
+                    const uint32_t put = pos < uint32_t(kListCap) ? min(k, uint32_t(kListCap) - pos) : 0u;
+                    uint32_t rest = sel;
+                    for (uint32_t i = 0; i < put; ++i) {
+                        const uint32_t b = __ffs(rest) - 1u;
+                        rest &= rest - 1u;
+                        s_list[pos + i] = w * 32u + b;
+                        taken |= 1u << b;
+                    }
+                    while (rest) {  // list full: stays active for a later sweep
+                        const uint32_t b = __ffs(rest) - 1u;
+                        rest &= rest - 1u;
+                        dmin = min(dmin, varr[w * 32u + b]);
+                    }
                 }
-                while (rest) {  // list full: stays active for a later sweep
-                    const uint32_t b = __ffs(rest) - 1u;
-                    rest &= rest - 1u;
-                    dmin = min(dmin, varr[w * 32u + b]);
-                }
-                cur[w] = word & ~taken;
+                bmD[w] = word & ~taken;
+                ndef += __popc(word & ~taken);
             }
-            dmin = __reduce_min_sync(0xFFFFFFFFu, dmin);
-            if (lane == 0 && dmin < kInf) atomicMin(&s_tmin[nb], dmin);
+            if (window < kInf) {
+                dmin = __reduce_min_sync(0xFFFFFFFFu, dmin);
+                if (lane == 0 && dmin < kInf) atomicMin(&s_tmin[t_nxt], dmin);
+            }
+            ndef = __reduce_add_sync(0xFFFFFFFFu, ndef);
+            if (lane == 0 && ndef) atomicAdd(&s_more[p], ndef);
             __syncthreads();
-            const uint32_t F = min(s_cnt, uint32_t(kListCap));
+            if (tid == 0) {  // slots of the next sweep: everyone is past their last read
+                s_cnt[p ^ 1u] = 0;
+                s_more[p ^ 1u] = 0;
+                s_tmin[(sweeps + 2u) % 3u] = kInf;
+            }
+            const uint32_t F = min(s_cnt[p], uint32_t(kListCap));
             // ---- 2. warp-level flattened (vertex, type) pairs; a warp takes g
             // consecutive list entries so that small frontiers still spread
             // over all warps
             const uint32_t g = min(32u, max(1u, (F + kCtaWarps - 1u) / kCtaWarps));
+            uint32_t nimpr = 0;
             for (uint32_t k0 = wid * g; k0 < F; k0 += kCtaWarps * g) {
                 const uint32_t j = k0 + lane;
                 uint32_t x = 0, p0 = 0, nt = 0;
@@ -222,32 +258,19 @@ __global__ void __launch_bounds__(kCtaThreads, 2048 / kCtaThreads) k_query_cta(D
                     if (cand < av) {
                         const uint32_t old = atomicMin(arr + tr.v, cand);
                         if (cand < old) {
-                            atomicOr(nxt + (tr.v >> 5), 1u << (tr.v & 31u));
-                            if (window < kInf) atomicMin(&s_tmin[nb], cand);
+                            atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
+                            if (window < kInf) atomicMin(&s_tmin[t_nxt], cand);
+                            ++nimpr;
                             if (COUNT) ++c_impr;
                         }
                     }
                 }
             }
+            nimpr = __reduce_add_sync(0xFFFFFFFFu, nimpr);
+            if (lane == 0 && nimpr) atomicAdd(&s_more[p], nimpr);
             __syncthreads();
-            // ---- 3. next frontier = improved + deferred
-            int any = 0;
-            for (uint32_t i = tid; i < W; i += kCtaThreads) {
-                const uint32_t v = nxt[i] | cur[i];
-                nxt[i] = v;
-                cur[i] = 0;
-                any |= v != 0u;
-            }
-            if (tid == 0) {
-                s_cnt = 0;
-                s_tmin[sweeps & 1u] = kInf;  // slot for the sweep after next
-            }
-            any = __syncthreads_or(any);
-            uint32_t *tmp = cur;
-            cur = nxt;
-            nxt = tmp;
             ++sweeps;
-            if (!any) break;
+            if (s_more[p] == 0u) break;  // nothing deferred, nothing lowered: fixpoint
         }
         // Output in caller ids
         for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = varr[__ldg(ix.perm + i)];
@@ -475,7 +498,7 @@ cudaError_t launch_grid_sw(const DevIndex &ix, const GridWork &w, uint32_t s, ui
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_grid<SW, SCHED>, kGridThreads, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    per_sm = std::min(per_sm, 4);
+    per_sm = std::min(per_sm, grid_ctas_per_sm());
     dim3 grid(unsigned(sms * per_sm)), block(kGridThreads);
     e = cudaMemsetAsync(w.ctl + 4, 0, 2 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;

@@ -52,6 +52,9 @@ cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_
 cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,
                               uint32_t t_s, uint32_t *d_out, cudaStream_t st);
 
+// CTAs per SM of the persistent grid kernels (env EAT_GRID_CTAS_PER_SM, default 4).
+int grid_ctas_per_sm();
+
 // Occupancy-derived grid size of the CTA kernel variant for n vertices (0 if arr does not fit).
 int cta_grid_size(uint32_t n, int variant);
 

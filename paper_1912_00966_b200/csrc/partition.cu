@@ -128,7 +128,7 @@ cudaError_t launch_round_sw(const DevIndex &ix, const PartWork &w, uint32_t lo, 
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_part_round<SW>, kPartThreads, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    per_sm = std::min(per_sm, 4);
+    per_sm = std::min(per_sm, grid_ctas_per_sm());
     DevIndex ixc = ix;
     PartWork wc = w;
     int f = first ? 1 : 0;

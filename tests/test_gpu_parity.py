@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_1912_00966_b200 import Engine, EatError, _lib  # noqa: E402
 
-KERNELS = ["cta", "frontier", "full_sweep"]
+KERNELS = ["cta", "frontier", "full_sweep", "async"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -75,7 +75,7 @@ def test_lookup_kernel_vs_get_connection(name, cs):
 
 # ----------------------------------------------------------------------------- single queries
 @pytest.mark.parametrize("kernel", KERNELS)
-@pytest.mark.parametrize("subwarp", [1, 8, 32])
+@pytest.mark.parametrize("subwarp", [0, 1, 8, 64])
 def test_tiny_single_queries(kernel, subwarp):
     tt = synth.generate("tiny")
     eng = Engine.from_timetable(tt, kernel=kernel, subwarp=subwarp)
@@ -96,7 +96,8 @@ def test_random_small_instances(kernel):
     for seed in range(400 if kernel != "full_sweep" else 150):
         tt = synth.random_small(seed)
         eng = Engine.from_timetable(tt, kernel=kernel, cluster_seconds=[3600, 600, 4096, 60][seed % 4],
-                                    subwarp=[1, 2, 4, 8, 16, 32][seed % 6])
+                                    subwarp=[1, 2, 4, 8, 16, 32, 0, 64][seed % 8],
+                                    cta_threads=[256, 384, 512][seed % 3])
         csa = oracle.CSA(tt.num_vertices, *tt.arrays())
         rng = np.random.default_rng(seed)
         for _ in range(3):
@@ -202,10 +203,14 @@ def test_metro_single_query():
     """BASELINE configs[3]: metro network, global e[] (frontier kernel)."""
     tt = synth.generate("metro")
     eng = Engine.from_timetable(tt)
-    assert eng.stats()["kernel_name"] in ("frontier", "cta")
+    assert eng.stats()["kernel_name"] in ("frontier", "cta", "async")
     csa = oracle.CSA(tt.num_vertices, *tt.arrays())
     for s, t_s in [synth.SINGLE_QUERY, (777, 30000)]:
         _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"metro ({s},{t_s})")
+    for kernel in ("frontier", "async"):
+        e2 = Engine.from_timetable(tt, kernel=kernel)
+        for s, t_s in [synth.SINGLE_QUERY, (91, 50000)]:
+            _assert_rows(e2.query(s, t_s), csa.query(s, t_s), f"metro {kernel} ({s},{t_s})")
 
 
 # ----------------------------------------------------------------------------- edge partition
@@ -246,7 +251,7 @@ def test_window_schedules_same_fixpoint(window):
     fixpoint, and so e[], is identical for every window."""
     tt = synth.generate("tiny")
     csa = oracle.CSA(tt.num_vertices, *tt.arrays())
-    eng = Engine.from_timetable(tt, window=window if window else 0x7FFFFFFF)
+    eng = Engine.from_timetable(tt, window=window if window else 0x7FFFFFFF, cta_threads=[256, 384, 512][window % 3])
     src, ts = synth.queries(tt, 50, 4)
     _assert_rows(eng.query_many(src, ts), csa.query_many(src, ts), f"window {window}")
     for seed in range(60):
