@@ -5,4 +5,4 @@ a C-ABI library (libeat.so: host compressor + sm_100a CUDA kernels + NCCL
 edge-partition driver, include/eat.h) with a thin Python binding.
 """
 from ._lib import EAT_INF, EatError  # noqa: F401
-from .engine import Engine  # noqa: F401
+from .engine import Engine, pinned_empty  # noqa: F401

@@ -11,6 +11,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "eat.h"
@@ -91,9 +92,12 @@ struct eat_handle {
     uint32_t *d_rounds1 = nullptr;   // async kernel: exchange rounds of the last query
     unsigned long long *d_counter = nullptr, *d_invalid = nullptr;
     unsigned long long *d_work = nullptr;  // EAT_BUILD_COUNTERS: 6 work counters
-    // batched scratch
-    uint32_t *d_bsrc = nullptr, *d_bts = nullptr, *d_bout = nullptr;
-    uint64_t bcap = 0;
+    // batched scratch: two pipeline stages (stream, queries, output rows, query counter, host staging)
+    cudaStream_t bstream[2] = {nullptr, nullptr};
+    uint32_t *d_bsrc[2] = {nullptr, nullptr}, *d_bts[2] = {nullptr, nullptr}, *d_bout[2] = {nullptr, nullptr};
+    uint32_t *h_stage[2] = {nullptr, nullptr};
+    unsigned long long *d_bcounter = nullptr;  // [2]
+    uint64_t bcap = 0, stage_cap = 0;
     int cta_grid = 0;
     // edge partition
     uint32_t part_rank = 0, part_count = 1, part_lo = 0, part_hi = 0;
@@ -109,7 +113,8 @@ void release_device(eat_handle *h) {
     cudaSetDevice(h->device);
     void *ptrs[] = {h->d_perm,  h->gw.arr, h->gw.q0,     h->gw.q1,      h->gw.stamp,   h->gw.bm,
                     h->gw.ctl,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
-                    h->d_bsrc,  h->d_bts,  h->d_bout,    h->d_work, h->d_rounds1};
+                    h->d_bsrc[0], h->d_bts[0], h->d_bout[0], h->d_bsrc[1], h->d_bts[1], h->d_bout[1],
+                    h->d_bcounter, h->d_work, h->d_rounds1};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     eat::async_free(h->aw);
@@ -120,6 +125,10 @@ void release_device(eat_handle *h) {
         eat::part_free(sl.pw);
     }
     if (h->h_out1) cudaFreeHost(h->h_out1);
+    for (int i = 0; i < 2; ++i) {
+        if (h->h_stage[i]) cudaFreeHost(h->h_stage[i]);
+        if (h->bstream[i]) cudaStreamDestroy(h->bstream[i]);
+    }
     if (h->comm) ncclCommDestroy(h->comm);
     if (h->stream) cudaStreamDestroy(h->stream);
 }
@@ -507,32 +516,28 @@ eat_status eat_query(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *out_arr)
     return EAT_OK;
 }
 
-eat_status eat_query_many_device(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
-                                 uint32_t *d_out, void *cuda_stream) {
-    if (!h) return fail(EAT_EINVAL, "NULL handle");
-    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
-    if (nq == 0) return EAT_OK;
-    if (!d_sources || !d_times || !d_out) return fail(EAT_EINVAL, "NULL argument");
-    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
-        return fail(EAT_ESTATE, "batched queries need a replicated handle (query-parallel sharding)");
-    std::lock_guard<std::mutex> lk(h->mu);
-    CUDA_TRY(cudaSetDevice(h->device));
-    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+}  // extern "C"
+
+namespace {
+
+// Enqueue a batch of device-resident queries on st (CTA kernel), or, when e[]
+// does not fit shared memory, one single-query launch after another.
+eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
+                         uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter) {
     if (h->cta_grid > 0) {
-        CUDA_TRY(eat::launch_query_cta(h->ix, int(h->subwarp), d_sources, d_times, nq, d_out, nullptr, h->d_counter,
+        CUDA_TRY(eat::launch_query_cta(h->ix, int(h->subwarp), d_sources, d_times, nq, d_out, nullptr, d_qcounter,
                                        h->d_invalid, 0, h->d_work, st));
         return EAT_OK;
     }
-    // |V| too large for shared memory: one grid-wide query after another
     std::vector<uint32_t> hs(nq), ht(nq);
     CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sources, nq * 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(ht.data(), d_times, nq * 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<uint32_t> inf;
     for (uint64_t q = 0; q < nq; ++q) {
         uint32_t *row = d_out + q * uint64_t(h->hx.n);
         if (hs[q] >= h->hx.n || ht[q] >= EAT_INF) {
-            CUDA_TRY(cudaMemsetAsync(row, 0xFF, h->hx.n * 4ull, st));  // 0xFFFFFFFF then fixed below
-            std::vector<uint32_t> inf(h->hx.n, EAT_INF);
+            if (inf.empty()) inf.assign(h->hx.n, EAT_INF);
             CUDA_TRY(cudaMemcpyAsync(row, inf.data(), h->hx.n * 4ull, cudaMemcpyHostToDevice, st));
             CUDA_TRY(cudaStreamSynchronize(st));
             continue;
@@ -543,46 +548,108 @@ eat_status eat_query_many_device(eat_handle *h, const uint32_t *d_sources, const
     return EAT_OK;
 }
 
+// Parallel host copy (staging -> caller memory).
+void host_copy(void *dst, const void *src, size_t bytes) {
+    const size_t nt = std::min<size_t>(8, std::max<size_t>(1, bytes >> 22));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < nt; ++t) {
+        const size_t a = bytes * t / nt, b = bytes * (t + 1) / nt;
+        th.emplace_back([=] { std::memcpy(static_cast<char *>(dst) + a, static_cast<const char *>(src) + a, b - a); });
+    }
+    for (auto &x : th) x.join();
+}
+
+}  // namespace
+
+extern "C" {
+
+eat_status eat_query_many_device(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
+                                 uint32_t *d_out, void *cuda_stream) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
+    if (nq == 0) return EAT_OK;
+    if (!d_sources || !d_times || !d_out) return fail(EAT_EINVAL, "NULL argument");
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
+        return fail(EAT_ESTATE, "batched queries need a replicated handle (query-parallel sharding)");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_TRY(cudaSetDevice(h->device));
+    return enqueue_batch(h, d_sources, d_times, nq, d_out, static_cast<cudaStream_t>(cuda_stream), h->d_counter);
+}
+
 eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t *times, uint64_t nq,
                           uint32_t *out) {
     if (!h) return fail(EAT_EINVAL, "NULL handle");
     if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
     if (nq == 0) return EAT_OK;
     if (!sources || !times || !out) return fail(EAT_EINVAL, "NULL argument");
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
+        return fail(EAT_ESTATE, "batched queries need a replicated handle (query-parallel sharding)");
     for (uint64_t q = 0; q < nq; ++q) {
         if (sources[q] >= h->hx.n) return fail(EAT_EINVAL, "invalid source vertex id at index " + std::to_string(q));
         if (times[q] >= EAT_INF) return fail(EAT_ERANGE, "t_s >= EAT_INF at index " + std::to_string(q));
     }
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_TRY(cudaSetDevice(h->device));
     const uint64_t n = h->hx.n;
-    // chunk so that the device output buffer stays <= 1 GiB
-    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(nq, (1ull << 30) / (4 * n)));
-    {
-        std::lock_guard<std::mutex> lk(h->mu);
-        CUDA_TRY(cudaSetDevice(h->device));
-        if (h->bcap < chunk) {
-            if (h->d_bsrc) cudaFree(h->d_bsrc);
-            if (h->d_bts) cudaFree(h->d_bts);
-            if (h->d_bout) cudaFree(h->d_bout);
-            h->d_bsrc = h->d_bts = h->d_bout = nullptr;
-            h->bcap = 0;
-            CUDA_TRY(cudaMalloc(&h->d_bsrc, chunk * 4));
-            CUDA_TRY(cudaMalloc(&h->d_bts, chunk * 4));
-            CUDA_TRY(cudaMalloc(&h->d_bout, chunk * n * 4));
-            h->bcap = chunk;
+    // Two-stage pipeline over chunks of queries (stream i&1): H2D queries ->
+    // batched kernel -> D2H rows, so chunk i+1 computes while chunk i copies.
+    // Output rows go straight to `out` when it is pinned (page-locked) host
+    // memory, else through pinned staging buffers and a parallel host copy.
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const uint64_t chunk =
+        std::max<uint64_t>(1, std::min<uint64_t>(nq, std::min<uint64_t>(1024, (256ull << 20) / (4 * n))));
+    if (!h->bstream[0])
+        for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&h->bstream[i], cudaStreamNonBlocking));
+    if (!h->d_bcounter) CUDA_TRY(cudaMalloc(&h->d_bcounter, 2 * sizeof(unsigned long long)));
+    if (h->bcap < chunk) {
+        for (int i = 0; i < 2; ++i) {
+            void *ptrs[] = {h->d_bsrc[i], h->d_bts[i], h->d_bout[i]};
+            for (void *p : ptrs)
+                if (p) cudaFree(p);
+            h->d_bsrc[i] = h->d_bts[i] = h->d_bout[i] = nullptr;
         }
+        h->bcap = 0;
+        for (int i = 0; i < 2; ++i) {
+            CUDA_TRY(cudaMalloc(&h->d_bsrc[i], chunk * 4));
+            CUDA_TRY(cudaMalloc(&h->d_bts[i], chunk * 4));
+            CUDA_TRY(cudaMalloc(&h->d_bout[i], chunk * n * 4));
+        }
+        h->bcap = chunk;
     }
-    for (uint64_t q0 = 0; q0 < nq; q0 += chunk) {
-        const uint64_t c = std::min(chunk, nq - q0);
-        {
-            std::lock_guard<std::mutex> lk(h->mu);
-            CUDA_TRY(cudaMemcpyAsync(h->d_bsrc, sources + q0, c * 4, cudaMemcpyHostToDevice, h->stream));
-            CUDA_TRY(cudaMemcpyAsync(h->d_bts, times + q0, c * 4, cudaMemcpyHostToDevice, h->stream));
+    if (!pinned && h->stage_cap < chunk) {
+        for (int i = 0; i < 2; ++i) {
+            if (h->h_stage[i]) cudaFreeHost(h->h_stage[i]);
+            h->h_stage[i] = nullptr;
         }
-        eat_status e = eat_query_many_device(h, h->d_bsrc, h->d_bts, c, h->d_bout, h->stream);
-        if (e != EAT_OK) return e;
-        std::lock_guard<std::mutex> lk(h->mu);
-        CUDA_TRY(cudaMemcpyAsync(out + q0 * n, h->d_bout, c * n * 4, cudaMemcpyDeviceToHost, h->stream));
-        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        h->stage_cap = 0;
+        for (int i = 0; i < 2; ++i) CUDA_TRY(cudaMallocHost(&h->h_stage[i], chunk * n * 4));
+        h->stage_cap = chunk;
+    }
+    const uint64_t nchunks = (nq + chunk - 1) / chunk;
+    for (uint64_t i = 0; i <= nchunks; ++i) {
+        if (i < nchunks) {
+            const int b = int(i & 1);
+            const uint64_t q0 = i * chunk, c = std::min(chunk, nq - q0);
+            cudaStream_t st = h->bstream[b];
+            CUDA_TRY(cudaMemcpyAsync(h->d_bsrc[b], sources + q0, c * 4, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(h->d_bts[b], times + q0, c * 4, cudaMemcpyHostToDevice, st));
+            eat_status e = enqueue_batch(h, h->d_bsrc[b], h->d_bts[b], c, h->d_bout[b], st, h->d_bcounter + b);
+            if (e != EAT_OK) return e;
+            CUDA_TRY(cudaMemcpyAsync(pinned ? out + q0 * n : h->h_stage[b], h->d_bout[b], c * n * 4,
+                                     cudaMemcpyDeviceToHost, st));
+        }
+        if (i >= 1) {  // retire chunk i-1 (its stage is reused by chunk i+1)
+            const int b = int((i - 1) & 1);
+            const uint64_t q0 = (i - 1) * chunk, c = std::min(chunk, nq - q0);
+            CUDA_TRY(cudaStreamSynchronize(h->bstream[b]));
+            if (!pinned) host_copy(out + q0 * n, h->h_stage[b], c * n * 4);
+        }
     }
     return EAT_OK;
 }

@@ -31,6 +31,15 @@ def _stream_ptr(stream) -> int:
     return int(s.cuda_stream)
 
 
+def pinned_empty(shape, dtype=np.uint32) -> np.ndarray:
+    """Page-locked host array (torch pinned storage viewed as NumPy)."""
+    import torch
+
+    t = torch.empty(int(np.prod(shape)) * np.dtype(dtype).itemsize, dtype=torch.uint8, pin_memory=True)
+    arr = t.numpy().view(dtype).reshape(shape)
+    return arr
+
+
 class Engine:
     """A built EAT index on one device (or one edge partition of it)."""
 
@@ -90,11 +99,18 @@ class Engine:
         _lib.eat_query(self._h, int(s), int(t_s), out.ctypes.data)
         return out
 
-    def query_many(self, sources, times) -> np.ndarray:
+    def query_many(self, sources, times, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """[nq, |V|] uint32.  `out` may be a preallocated C-contiguous uint32
+        array, e.g. from ``pinned_empty`` (page-locked: rows are copied
+        straight from the device; pageable memory goes through pinned staging)."""
         src, ts = _u32(sources), _u32(times)
         if src.shape != ts.shape:
             raise ValueError("sources and times must have equal length")
-        out = np.empty((src.shape[0], self.num_vertices), dtype=np.uint32)
+        shape = (src.shape[0], self.num_vertices)
+        if out is None:
+            out = np.empty(shape, dtype=np.uint32)
+        elif out.shape != shape or out.dtype != np.uint32 or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a C-contiguous uint32 array of shape {shape}")
         _lib.eat_query_many(self._h, src.ctypes.data, ts.ctypes.data, src.shape[0], out.ctypes.data)
         return out
 

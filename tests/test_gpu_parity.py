@@ -183,8 +183,16 @@ def test_city_batch_full_size_sampled():
     rows = np.random.default_rng(7).choice(src.size, 120, replace=False)
     got = out[torch.tensor(rows, device="cuda")].cpu().numpy().astype(np.uint32)
     _assert_rows(got, csa.query_many(src[rows], ts[rows]), "city batch sampled rows")
-    # host e2e path on a slice
-    _assert_rows(eng.query_many(src[:200], ts[:200]), csa.query_many(src[:200], ts[:200]), "city batch host")
+    # host e2e paths (pageable -> pinned staging; pinned -> direct), several pipeline chunks
+    want = csa.query_many(src[:2500:5], ts[:2500:5])
+    _assert_rows(eng.query_many(src[:2500:5], ts[:2500:5]), want, "city batch host pageable")
+    from paper_1912_00966_b200 import pinned_empty
+
+    pin = pinned_empty((500, tt.num_vertices))
+    _assert_rows(eng.query_many(src[:2500:5], ts[:2500:5], out=pin), want, "city batch host pinned")
+    full = pinned_empty((src.size, tt.num_vertices))
+    eng.query_many(src, ts, out=full)
+    _assert_rows(full[rows], csa.query_many(src[rows], ts[rows]), "city batch host pinned, all 10k")
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
