@@ -284,7 +284,9 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     h->st.smem_vertices_max = uint32_t(avail * 32 / (4 * 32 + 2 * 4));
     uint32_t k = requested;
     const bool async_ok = eat::async_parts(h->hx.n) > 0;
-    if (k == EAT_KERNEL_AUTO) k = h->cta_grid > 0 ? EAT_KERNEL_CTA : (async_ok ? EAT_KERNEL_ASYNC : EAT_KERNEL_FRONTIER);
+    // AUTO: the CTA kernel when e[] fits shared memory, else the grid frontier
+    // kernel (measured faster than ASYNC on metro/country)
+    if (k == EAT_KERNEL_AUTO) k = h->cta_grid > 0 ? EAT_KERNEL_CTA : EAT_KERNEL_FRONTIER;
     if (k == EAT_KERNEL_CTA && h->cta_grid == 0)
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
     if (k == EAT_KERNEL_ASYNC && !async_ok)
