@@ -67,7 +67,7 @@ typedef struct eat_timetable {
     const uint32_t *v;            /* [num_connections] target vertex  (< num_vertices) */
     const uint32_t *dep;          /* [num_connections] departure t at u, seconds */
     const uint32_t *dur;          /* [num_connections] duration lambda, seconds; dep+dur < EAT_INF */
-    const uint32_t *trip;         /* optional (NULL): trip id per connection (reserved) */
+    const uint32_t *trip;         /* optional (NULL): trip id per connection (needed by opts.subtrips) */
     const float *xy;              /* optional (NULL): [2*num_vertices] stop coordinates */
 } eat_timetable;
 
@@ -120,6 +120,10 @@ typedef struct eat_build_opts {
                                      Results are identical for every value (same fixpoint). */
     uint32_t cta_threads;         /* CTA kernel threads per query: 0 -> 256; 512, 384 or 256 (occupancy knob,
                                      tools/sweep_cta.py) */
+    uint32_t subtrips;            /* sub-trip shortcuts (needs tt->trip): 0 off;
+                                     1 = r = round(sqrt(k)) per trip of k connections;
+                                     2 = r = round(sqrt(average trip length)); >= 3: r itself.
+                                     Arrival times are unchanged; sweeps (hops) drop. */
 } eat_build_opts;
 
 #define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */
@@ -198,6 +202,7 @@ typedef struct eat_stats {
     uint64_t spill_items_read;    /* out-of-line AP items read */
     uint64_t improvements;        /* successful atomicMin relaxations */
     uint64_t sweeps_total;        /* relaxation sweeps summed over queries */
+    uint64_t num_shortcuts;       /* sub-trip shortcut connections added at build (indexed with the rest) */
 } eat_stats;
 
 eat_status eat_get_stats(const eat_handle *h, eat_stats *out);

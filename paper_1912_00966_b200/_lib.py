@@ -44,7 +44,7 @@ class eat_build_opts(ctypes.Structure):
                 ("kernel", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("subwarp", ctypes.c_uint32),
                 ("mode", ctypes.c_uint32), ("part_rank", ctypes.c_uint32), ("part_count", ctypes.c_uint32),
                 ("nccl_unique_id", ctypes.c_void_p), ("window_seconds", ctypes.c_uint32),
-                ("cta_threads", ctypes.c_uint32)]
+                ("cta_threads", ctypes.c_uint32), ("subtrips", ctypes.c_uint32)]
 
 
 class eat_stats(ctypes.Structure):
@@ -58,7 +58,7 @@ class eat_stats(ctypes.Structure):
                 ("smem_vertices_max", ctypes.c_uint32), ("vertex_visits", ctypes.c_uint64),
                 ("type_evals", ctypes.c_uint64), ("cluster_reads", ctypes.c_uint64),
                 ("spill_items_read", ctypes.c_uint64), ("improvements", ctypes.c_uint64),
-                ("sweeps_total", ctypes.c_uint64)]
+                ("sweeps_total", ctypes.c_uint64), ("num_shortcuts", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

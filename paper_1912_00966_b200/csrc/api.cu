@@ -318,7 +318,10 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
     if (h->kernel == EAT_KERNEL_CTA) {
         uint32_t q[2] = {s, t_s};
         CUDA_TRY(cudaMemcpyAsync(h->d_q1, q, sizeof(q), cudaMemcpyHostToDevice, st));
-        CUDA_TRY(eat::launch_query_cta(h->ix, int(h->subwarp), h->d_q1, h->d_q1 + 1, 1, d_out, h->d_sweeps1,
+        // a lone query gets the widest CTA (1024 threads): it has the SM to itself
+        eat::DevIndex ix1 = h->ix;
+        ix1.cta_threads = 1024;
+        CUDA_TRY(eat::launch_query_cta(ix1, int(h->subwarp), h->d_q1, h->d_q1 + 1, 1, d_out, h->d_sweeps1,
                                        h->d_counter, h->d_invalid, 1, nullptr, st));
     } else if (h->kernel == EAT_KERNEL_ASYNC) {
         CUDA_TRY(eat::launch_query_async(h->ix, h->aw, s, t_s, d_out, st));
@@ -370,10 +373,22 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 && !o.nccl_unique_id;
     h->host_only = (o.flags & EAT_BUILD_HOST_ONLY) != 0;
     std::string msg;
-    int rc;
+    int rc = EAT_OK;
+    eat::SubtripStats sts;
     try {
-        rc = eat::build_host_index(tt->num_vertices, tt->num_connections, tt->u, tt->v, tt->dep, tt->dur, tt->xy,
-                                   p, h->hx, msg);
+        if (o.subtrips) {
+            // NEXT-1 data enhancement: index the timetable
+            // plus sub-trip shortcuts; arrival times are unchanged
+            std::vector<uint32_t> U, V, D, L;
+            rc = eat::make_subtrips(tt->num_connections, tt->u, tt->v, tt->dep, tt->dur, tt->trip, o.subtrips, U, V,
+                                    D, L, sts, msg);
+            if (rc == EAT_OK)
+                rc = eat::build_host_index(tt->num_vertices, U.size(), U.data(), V.data(), D.data(), L.data(), tt->xy,
+                                           p, h->hx, msg);
+        } else {
+            rc = eat::build_host_index(tt->num_vertices, tt->num_connections, tt->u, tt->v, tt->dep, tt->dur, tt->xy,
+                                       p, h->hx, msg);
+        }
     } catch (const std::bad_alloc &) {
         rc = EAT_ENOMEM;
         msg = "out of host memory during build";
@@ -385,7 +400,8 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     eat_stats &s = h->st;
     s.num_vertices = h->hx.n;
     s.num_clusters = h->hx.num_clusters;
-    s.num_connections = h->hx.m;
+    s.num_connections = tt->num_connections;
+    s.num_shortcuts = sts.shortcuts;
     s.num_types = h->hx.num_types;
     s.num_edges = h->hx.num_edges;
     s.num_cluster_records = h->hx.num_crec;

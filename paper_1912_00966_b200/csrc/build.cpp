@@ -189,6 +189,116 @@ struct Chunk {
 
 }  // namespace
 
+// ---------------------------------------------------------------- sub-trips
+// Data enhancement of PAPER.md:342-354 (Sec. II-G): every trip, a sequence of
+// connections (v_1,v_2,t_1,l_1), ..., (v_k,v_{k+1},t_k,l_k) with
+// t_i + l_i <= t_{i+1}, is cut into consecutive, non-overlapping
+// sub-trips of r connections (the last one k % r); a sub-trip
+// (v_i..v_{j+1}) adds the shortcut (v_i, v_{j+1}, t_i, t_j + l_j - t_i).
+// A shortcut's arrival is the arrival of the vehicle itself, so earliest
+// arrival times are unchanged; paths get fewer hops, so sweeps drop.
+// scheme 1: r = round(sqrt(k)) per trip; scheme 2: r =
+// round(sqrt(average trip length)); scheme >= 3: r = scheme.
+// Connections of a trip are ordered by departure (ties: input order); a trip
+// that does not chain (v_i != u_{i+1} or t_i + l_i > t_{i+1}) gets no shortcut.
+int make_subtrips(uint64_t m, const uint32_t *u, const uint32_t *v, const uint32_t *dep, const uint32_t *dur,
+                  const uint32_t *trip, uint32_t scheme, std::vector<uint32_t> &U, std::vector<uint32_t> &V,
+                  std::vector<uint32_t> &D, std::vector<uint32_t> &L, SubtripStats &st, std::string &msg) {
+    st = SubtripStats{};
+    if (!trip) {
+        msg = "sub-trips need the timetable's trip ids (eat_timetable.trip)";
+        return EAT_EINVAL;
+    }
+    // order connections by (trip, dep, input index): counting sort by trip id
+    // when ids are dense, else a comparison sort
+    uint32_t tmax = 0;
+    for (uint64_t i = 0; i < m; ++i) tmax = std::max(tmax, trip[i]);
+    std::vector<uint64_t> order(m);
+    std::vector<uint64_t> tptr;
+    if (m && uint64_t(tmax) <= 4 * m + 16) {
+        tptr.assign(uint64_t(tmax) + 2, 0);
+        for (uint64_t i = 0; i < m; ++i) tptr[trip[i] + 1]++;
+        for (uint64_t t = 0; t <= tmax; ++t) tptr[t + 1] += tptr[t];
+        std::vector<uint64_t> fill(tptr.begin(), tptr.end() - 1);
+        for (uint64_t i = 0; i < m; ++i) order[fill[trip[i]]++] = i;
+    } else {
+        std::iota(order.begin(), order.end(), uint64_t(0));
+        std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return trip[a] < trip[b]; });
+        tptr.push_back(0);
+        for (uint64_t i = 1; i <= m; ++i)
+            if (i == m || trip[order[i]] != trip[order[i - 1]]) tptr.push_back(i);
+    }
+    const uint64_t ntrips = tptr.size() - 1;
+    // per trip: stable sort by departure, chain check
+    std::vector<uint8_t> ok(ntrips, 0);
+    std::atomic<uint64_t> sum_len(0), n_ok(0);
+    parallel_chunks(ntrips, [&](uint64_t lo, uint64_t hi) {
+        uint64_t sl = 0, no = 0;
+        for (uint64_t t = lo; t < hi; ++t) {
+            const uint64_t a = tptr[t], b = tptr[t + 1];
+            if (b - a < 2) continue;
+            std::stable_sort(order.begin() + a, order.begin() + b, [&](uint64_t x, uint64_t y) { return dep[x] < dep[y]; });
+            bool good = true;
+            for (uint64_t i = a; i + 1 < b && good; ++i) {
+                const uint64_t c = order[i], d = order[i + 1];
+                good = v[c] == u[d] && uint64_t(dep[c]) + dur[c] <= dep[d];
+            }
+            if (good) {
+                ok[t] = 1;
+                sl += b - a;
+                ++no;
+            }
+        }
+        sum_len += sl;
+        n_ok += no;
+    });
+    st.trips = ntrips;
+    st.chained = n_ok.load();
+    const double avg = st.chained ? double(sum_len.load()) / double(st.chained) : 0.0;
+    const uint32_t r_global = scheme == 2 ? uint32_t(std::lround(std::sqrt(avg))) : (scheme >= 3 ? scheme : 0);
+    st.r_global = r_global;
+    // emit shortcuts (count first, then fill, in trip order)
+    auto r_of = [&](uint64_t k) -> uint64_t { return scheme == 1 ? uint64_t(std::llround(std::sqrt(double(k)))) : r_global; };
+    std::vector<uint64_t> cnt(ntrips + 1, 0);
+    parallel_chunks(ntrips, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t t = lo; t < hi; ++t) {
+            if (!ok[t]) continue;
+            const uint64_t k = tptr[t + 1] - tptr[t], r = r_of(k);
+            if (r < 2) continue;
+            cnt[t + 1] = k / r + ((k % r) >= 2 ? 1 : 0);
+        }
+    });
+    for (uint64_t t = 0; t < ntrips; ++t) cnt[t + 1] += cnt[t];
+    const uint64_t S = cnt[ntrips];
+    st.shortcuts = S;
+    U.resize(m + S);
+    V.resize(m + S);
+    D.resize(m + S);
+    L.resize(m + S);
+    std::copy(u, u + m, U.begin());
+    std::copy(v, v + m, V.begin());
+    std::copy(dep, dep + m, D.begin());
+    std::copy(dur, dur + m, L.begin());
+    parallel_chunks(ntrips, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t t = lo; t < hi; ++t) {
+            if (!ok[t] || cnt[t + 1] == cnt[t]) continue;
+            const uint64_t a = tptr[t], k = tptr[t + 1] - a, r = r_of(k);
+            uint64_t o = m + cnt[t];
+            for (uint64_t i = 0; i < k; i += r) {
+                const uint64_t j = std::min(k, i + r) - 1;  // sub-trip = connections i..j
+                if (j == i) continue;
+                const uint64_t ci = order[a + i], cj = order[a + j];
+                U[o] = u[ci];
+                V[o] = v[cj];
+                D[o] = dep[ci];
+                L[o] = dep[cj] + dur[cj] - dep[ci];
+                ++o;
+            }
+        }
+    });
+    return EAT_OK;
+}
+
 void partition_range(const HostIndex &ix, uint32_t rank, uint32_t count, uint32_t &lo, uint32_t &hi) {
     uint64_t T = ix.num_types;
     auto cut = [&](uint32_t r) -> uint32_t {

@@ -75,6 +75,17 @@ struct BuildParams {
     uint32_t renumber = 0;
 };
 
+struct SubtripStats {
+    uint64_t trips = 0, chained = 0, shortcuts = 0;
+    uint32_t r_global = 0;
+};
+
+// Sub-trip shortcuts: U/V/D/L = the input connections
+// followed by one shortcut per sub-trip.  Returns 0 or an eat_status code.
+int make_subtrips(uint64_t m, const uint32_t *u, const uint32_t *v, const uint32_t *dep, const uint32_t *dur,
+                  const uint32_t *trip, uint32_t scheme, std::vector<uint32_t> &U, std::vector<uint32_t> &V,
+                  std::vector<uint32_t> &D, std::vector<uint32_t> &L, SubtripStats &st, std::string &msg);
+
 // Host compressor (build.cpp).  Returns 0 or an eat_status code; msg set on error.
 int build_host_index(uint32_t n, uint64_t m, const uint32_t *u, const uint32_t *v, const uint32_t *dep,
                      const uint32_t *dur, const float *xy, const BuildParams &p, HostIndex &out,

@@ -79,7 +79,7 @@ __global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *boun
 // Minimum resident CTAs per SM for the register budget: shared memory (e[]
 // of a 10k-stop city) already caps residency at 4 (512 threads) or 5.
 template <int T>
-constexpr int cta_min_blocks() { return T >= 512 ? 4 : 5; }
+constexpr int cta_min_blocks() { return T >= 1024 ? 1 : (T >= 512 ? 4 : 5); }
 
 template <bool COUNT, int kCtaThreads, int kListCap>
 __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
@@ -483,6 +483,7 @@ cudaError_t launch_cta_variant(int variant, const DevIndex &ix, const uint32_t *
                                uint32_t *out, uint32_t *sweeps, unsigned long long *qc, unsigned long long *inv,
                                int grid_cap, unsigned long long *counters, cudaStream_t st) {
     switch (variant) {
+        case 1024: return launch_cta_sw<COUNT, 1024, 2048>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
         case 384: return launch_cta_sw<COUNT, 384, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
         case 256: return launch_cta_sw<COUNT, 256, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
         default: return launch_cta_sw<COUNT, 512, 2048>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);

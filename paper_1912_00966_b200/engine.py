@@ -47,15 +47,18 @@ class Engine:
                  renumber: str = "auto", kernel: str = "auto", subwarp: int = 0, device: int = -1,
                  host_only: bool = False, counters: bool = False, mode: str = "replicated", part_rank: int = 0, part_count: int = 1,
                  nccl_unique_id: Optional[bytes] = None, window: int = 0,
-                 cta_threads: int = 0):
+                 cta_threads: int = 0, subtrips: int = 0, trip=None):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
         if any(a.shape[0] != m for a in arrs):
             raise ValueError("u, v, dep, dur must have equal length")
         xy_a = None if xy is None else np.ascontiguousarray(np.asarray(xy, dtype=np.float32).reshape(-1))
+        trip_a = None if trip is None else _u32(trip)
+        if trip_a is not None and trip_a.shape[0] != m:
+            raise ValueError("trip must have one id per connection")
         tt = _lib.eat_timetable(num_vertices=int(num_vertices), num_connections=int(m),
-                                u=_p(arrs[0]), v=_p(arrs[1]), dep=_p(arrs[2]), dur=_p(arrs[3]), trip=None,
+                                u=_p(arrs[0]), v=_p(arrs[1]), dep=_p(arrs[2]), dur=_p(arrs[3]), trip=_p(trip_a),
                                 xy=_p(xy_a, ctypes.c_float))
         self._nccl_buf = None
         if nccl_unique_id is not None:
@@ -66,13 +69,16 @@ class Engine:
                                    | (_lib.EAT_BUILD_COUNTERS if counters else 0), subwarp=int(subwarp),
                                    mode=_lib.EAT_MODE[mode], part_rank=int(part_rank), part_count=int(part_count),
                                    nccl_unique_id=ctypes.cast(self._nccl_buf, ctypes.c_void_p) if self._nccl_buf else None,
-                                   window_seconds=int(window), cta_threads=int(cta_threads))
+                                   window_seconds=int(window), cta_threads=int(cta_threads),
+                                   subtrips=int(subtrips))
         self._h = _lib.eat_build(tt, opts)
         self.num_vertices = int(num_vertices)
         self.num_connections = int(m)
 
     @classmethod
     def from_timetable(cls, tt, **kw) -> "Engine":
+        if kw.get("subtrips") and "trip" not in kw:
+            kw["trip"] = tt.trip
         return cls(tt.num_vertices, tt.u, tt.v, tt.dep, tt.dur, getattr(tt, "xy", None), **kw)
 
     # ------------------------------------------------------------------ lifecycle

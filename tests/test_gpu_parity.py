@@ -282,3 +282,18 @@ def test_country_single_query():
         eng = Engine.from_timetable(tt, **kw)
         _assert_rows(eng.query(*synth.SINGLE_QUERY), want, f"country {kw}")
         eng.close()
+
+
+@pytest.mark.parametrize("scheme", [1, 2])
+def test_subtrips_parity(scheme):
+    """NEXT-1: the index with sub-trip shortcuts gives the oracle's arrival
+    times of the ORIGINAL timetable (batched + single kernels)."""
+    for name in ("tiny", "city"):
+        tt = synth.generate(name)
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        src, ts = synth.queries(tt, 40, 5)
+        for kernel in ("cta", "frontier"):
+            eng = Engine.from_timetable(tt, subtrips=scheme, kernel=kernel)
+            assert eng.stats()["num_shortcuts"] > 0
+            _assert_rows(eng.query(*synth.SINGLE_QUERY), csa.query(*synth.SINGLE_QUERY), f"subtrips {name} {kernel}")
+        _assert_rows(eng.query_many(src, ts), csa.query_many(src, ts), f"subtrips {name} batch")

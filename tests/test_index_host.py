@@ -211,3 +211,66 @@ def test_partition_ranges_cover_vertices():
         assert cuts == sorted(cuts)
         owned = sum(int(tptr[cuts[r + 1]] - tptr[cuts[r]]) for r in range(P))
         assert owned == T
+
+
+def _expected_shortcuts(tt, scheme):
+    """Test-side statement of PAPER.md:349-354: trips ordered by departure,
+    blocks of r connections, one shortcut (v_i, v_{j+1}, t_i, t_j + l_j - t_i)
+    per block of >= 2 connections."""
+    import math
+
+    out = []
+    by_trip = {}
+    for i in range(tt.num_connections):
+        by_trip.setdefault(int(tt.trip[i]), []).append(i)
+    lens = []
+    trips = []
+    for t, idx in sorted(by_trip.items()):
+        idx.sort(key=lambda i: (int(tt.dep[i]), i))
+        ok = all(tt.v[a] == tt.u[b] and int(tt.dep[a]) + int(tt.dur[a]) <= int(tt.dep[b]) for a, b in zip(idx, idx[1:]))
+        if ok and len(idx) >= 2:
+            trips.append(idx)
+            lens.append(len(idx))
+    rg = round(math.sqrt(sum(lens) / len(lens))) if scheme == 2 else scheme
+    for idx in trips:
+        k = len(idx)
+        r = round(math.sqrt(k)) if scheme == 1 else rg
+        if r < 2:
+            continue
+        for i in range(0, k, r):
+            j = min(k, i + r) - 1
+            if j > i:
+                a, b = idx[i], idx[j]
+                out.append((int(tt.u[a]), int(tt.v[b]), int(tt.dur[b]) + int(tt.dep[b]) - int(tt.dep[a]), int(tt.dep[a])))
+    return out
+
+
+@pytest.mark.parametrize("scheme", [1, 2, 4])
+def test_subtrip_shortcuts_and_invariance(scheme):
+    """NEXT-1: the index holds the original connections
+    plus exactly the paper's shortcuts, and the oracle's arrival times on the
+    enhanced connection set equal those on the original one."""
+    tt = synth.generate("tiny")
+    eng = Engine.from_timetable(tt, host_only=True, subtrips=scheme)
+    ex = eng.export()
+    dec, _ = _decode(ex, 3600)
+    perm = ex["perm"].astype(np.int64)
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.shape[0])
+    got = Counter((int(inv[u]), int(inv[v]), lam, d) for (u, v, lam, d) in dec)
+    want = Counter(zip(tt.u.tolist(), tt.v.tolist(), tt.dur.tolist(), tt.dep.tolist()))
+    sc = Counter(_expected_shortcuts(tt, scheme))
+    assert got == want + sc
+    assert eng.stats()["num_shortcuts"] == sum(sc.values()) > 0
+    e = np.array([(u, v, d, lam) for (u, v, lam, d), c in got.items() for _ in range(c)], np.uint32)
+    enh = oracle.CSA(tt.num_vertices, e[:, 0], e[:, 1], e[:, 2], e[:, 3])
+    base = oracle.CSA(tt.num_vertices, *tt.arrays())
+    src, ts = synth.queries(tt, 30, 3)
+    assert np.array_equal(enh.query_many(src, ts), base.query_many(src, ts))
+
+
+def test_subtrips_need_trip_ids():
+    tt = synth.generate("tiny")
+    with pytest.raises(EatError) as e:
+        Engine(tt.num_vertices, tt.u, tt.v, tt.dep, tt.dur, host_only=True, subtrips=1)
+    assert e.value.status == _lib.EAT_EINVAL
