@@ -200,7 +200,7 @@ def run_single(args):
     t0 = time.perf_counter()
     tt = synth.generate(cfg)
     gen_s = time.perf_counter() - t0
-    kw = dict(kw)
+    kw = dict(kw, subtrips=args.subtrips)
     if kw.get("mode") == "edge_partitioned":
         kw.update(part_rank=rank, part_count=world, nccl_unique_id=nccl_unique_id() if world > 1 else None)
     t0 = time.perf_counter()
@@ -268,7 +268,8 @@ def run_single(args):
                            "connections": tt.num_connections, "edges": st0["num_edges"], "types": st0["num_types"],
                            "kernel": st0["kernel_name"], "mode": kw.get("mode", "replicated"),
                            "l2": "flushed (256 MiB write) between timed steps", "index_bytes": st0["index_bytes"],
-                           "generate_s": gen_s, "build_s": build_s},
+                           "generate_s": gen_s, "build_s": build_s, "subtrips": args.subtrips,
+                           "shortcuts": st0["num_shortcuts"]},
                 "sweeps": st["last_sweeps"], "rounds": st["last_rounds"],
                 "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8,
                         "d2h_bytes_per_step": tt.num_vertices * 4},
@@ -300,7 +301,7 @@ def run_gpu(args):
     per = nsrc * ntime
     src, ts = all_src[rank * per:(rank + 1) * per], all_ts[rank * per:(rank + 1) * per]
     nq = src.size
-    eng = Engine.from_timetable(tt, device=dev, kernel="auto")
+    eng = Engine.from_timetable(tt, device=dev, kernel="auto", subtrips=args.subtrips)
     st0 = eng.stats()
     stream = torch.cuda.Stream(device=dev)
     d_src = torch.tensor(src.astype(np.int32), device=dev)
@@ -342,6 +343,25 @@ def run_gpu(args):
         tot_ms = float(t.item())
     value = world * nq * args.steps / (tot_ms / 1e3)
 
+    # ---- the same batch without sub-trip shortcuts (plain Cluster-AP index)
+    variants = {}
+    if args.subtrips:
+        eng0 = Engine.from_timetable(tt, device=dev, kernel="auto", subtrips=0)
+        for _ in range(2):
+            eng0.query_many_device(d_src, d_ts, d_out, stream=stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ms0 = 0.0
+        for k in range(3):
+            with torch.cuda.stream(stream):
+                flush.fill_(k)
+                a.record(stream)
+                eng0.query_many_device(d_src, d_ts, d_out, stream=stream)
+                b.record(stream)
+            b.synchronize()
+            ms0 += a.elapsed_time(b)
+        variants["no_subtrips_queries_per_s_per_gpu"] = nq * 3 / (ms0 / 1e3)
+        eng0.close()
+
     # ---- e2e through the public API with host buffers: pinned host queries
     # in, every step H2D of the queries + kernel + D2H of all result rows into
     # pinned host memory (eat_query_many pipelines chunks over two streams)
@@ -371,7 +391,7 @@ def run_gpu(args):
     o1 = torch.empty(tt.num_vertices, dtype=torch.int32, device=dev)
     single = {}
     for kname in ("cta", "frontier"):
-        e1 = Engine.from_timetable(tt, device=dev, kernel=kname)
+        e1 = Engine.from_timetable(tt, device=dev, kernel=kname, subtrips=args.subtrips)
         for _ in range(3):
             e1.query_device(s1, t1, o1, stream=stream)
         stream.synchronize()
@@ -390,7 +410,7 @@ def run_gpu(args):
     try:
         from paper_1912_00966_b200 import counters
 
-        cnt = counters.count_batch(tt, src, ts, dev)
+        cnt = counters.count_batch(tt, src, ts, dev, subtrips=args.subtrips)
         alg_bytes = cnt["algorithmic_bytes"]
         mean_launch_s = (sum(step_ms) / len(step_ms)) / 1e3
         peak, peak_src = _peaks()
@@ -421,8 +441,10 @@ def run_gpu(args):
                        "stops": tt.num_vertices, "edges": st0["num_edges"], "connections": tt.num_connections,
                        "types": st0["num_types"], "queries_per_gpu": nq, "parallelism": f"query-sharded x{world}",
                        "l2": "flushed (256 MiB write) between timed steps", "kernel": st0["kernel_name"],
-                       "subwarp": 8},
+                       "subtrips": args.subtrips, "window_s": 1800, "cta_threads": 256,
+                       "shortcuts": st0["num_shortcuts"]},
             "connections_resolved_per_s": resolved / (tot_ms / 1e3),
+            "variants": variants,
             "single_query_ms": {k: v["ms"] for k, v in single.items()},
             "single_query_sweeps": {k: v["sweeps"] for k, v in single.items()},
             "single_query_config": "city, s=0, t_s=06:00 (BASELINE configs[1]), device time per query",
@@ -448,6 +470,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-queries", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--subtrips", type=int, default=2,
+                    help="sub-trip shortcut scheme (PAPER.md:342-354): 0 off, 1 sqrt(k) per trip, 2 sqrt(avg)")
     ap.add_argument("--workload", default="city_batch", choices=["city_batch"] + sorted(SINGLE_WORKLOADS))
     args = ap.parse_args()
     if args.warmup < 3:

@@ -169,6 +169,21 @@ eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t
 eat_status eat_query_many_device(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
                                  uint32_t *d_out, void *cuda_stream);
 
+/* Goal-directed EAT (NEXT-4; the goal-directed variant named in PAPER.md:60,
+ * 679): for i < nq, out[i] = earliest arrival time at dsts[i] for the query
+ * (sources[i], times[i]), EAT_INF if unreachable.  The search is the same
+ * relaxation, pruned: a vertex whose arrival is already >= the best known
+ * arrival at the target is dropped (every path through it arrives later).
+ * Host arrays; out has nq entries.  Errors as eat_query_many, plus EAT_EINVAL
+ * for dsts[i] >= num_vertices. */
+eat_status eat_query_many_target(eat_handle *h, const uint32_t *sources, const uint32_t *times,
+                                 const uint32_t *dsts, uint64_t nq, uint32_t *out);
+
+/* Same, device pointers on the handle's device, enqueued on cuda_stream;
+ * invalid (s, t_s, dst) triples yield EAT_INF and count in invalid_queries. */
+eat_status eat_query_many_target_device(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times,
+                                        const uint32_t *d_dsts, uint64_t nq, uint32_t *d_out, void *cuda_stream);
+
 /* Test/introspection entry point: the Cluster-AP lookup kernel alone
  * (PAPER.md:305-306 with Algorithm 6).  For i < n: d_out[i] = the smallest
  * departure >= d_bound[i] of internal connection type d_type[i], or EAT_INF.

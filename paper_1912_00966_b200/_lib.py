@@ -27,6 +27,7 @@ EAT_BUILD_COUNTERS = 0x2
 
 # symbols include/eat.h declares (checked by tests/test_abi.py)
 EXPORTED = ["eat_build", "eat_query", "eat_query_device", "eat_query_many", "eat_query_many_device",
+            "eat_query_many_target", "eat_query_many_target_device",
             "eat_lookup_device", "eat_get_stats", "eat_index_export", "eat_index_sizes", "eat_partition_range", "eat_free", "eat_last_error",
             "eat_abi_version"]
 
@@ -93,6 +94,12 @@ def lib() -> ctypes.CDLL:
         L.eat_query_many_device.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                                             ctypes.c_void_p]
         L.eat_query_many_device.restype = S
+        L.eat_query_many_target.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                            ctypes.c_void_p]
+        L.eat_query_many_target.restype = S
+        L.eat_query_many_target_device.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                   ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+        L.eat_query_many_target_device.restype = S
         L.eat_lookup_device.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                                         ctypes.c_void_p]
         L.eat_lookup_device.restype = S
@@ -140,6 +147,14 @@ def eat_query_many(h, src_ptr: int, ts_ptr: int, nq: int, out_ptr: int):
 
 def eat_query_many_device(h, d_src: int, d_ts: int, nq: int, d_out: int, stream: int):
     check(lib().eat_query_many_device(h, d_src, d_ts, nq, d_out, stream))
+
+
+def eat_query_many_target(h, src_ptr: int, ts_ptr: int, dst_ptr: int, nq: int, out_ptr: int):
+    check(lib().eat_query_many_target(h, src_ptr, ts_ptr, dst_ptr, nq, out_ptr))
+
+
+def eat_query_many_target_device(h, d_src: int, d_ts: int, d_dst: int, nq: int, d_out: int, stream: int):
+    check(lib().eat_query_many_target_device(h, d_src, d_ts, d_dst, nq, d_out, stream))
 
 
 def eat_lookup_device(h, d_type: int, d_bound: int, n: int, d_out: int, stream: int):

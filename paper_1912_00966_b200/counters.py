@@ -20,12 +20,12 @@ def bytes_from_counts(c: dict, nq: int, n: int) -> int:
                + 4 * c["spill_items_read"] + 8 * nq + 4 * n * nq)
 
 
-def count_batch(tt, src, ts, device: int) -> dict:
+def count_batch(tt, src, ts, device: int, **engine_kw) -> dict:
     import torch
 
     from .engine import Engine
 
-    eng = Engine.from_timetable(tt, device=device, counters=True)
+    eng = Engine.from_timetable(tt, device=device, counters=True, **engine_kw)
     d_src = torch.tensor(np.asarray(src, np.uint32).astype(np.int32), device=device)
     d_ts = torch.tensor(np.asarray(ts, np.uint32).astype(np.int32), device=device)
     out = torch.empty((d_src.numel(), tt.num_vertices), dtype=torch.int32, device=device)

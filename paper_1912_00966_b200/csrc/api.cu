@@ -598,6 +598,72 @@ eat_status eat_query_many_device(eat_handle *h, const uint32_t *d_sources, const
     return enqueue_batch(h, d_sources, d_times, nq, d_out, static_cast<cudaStream_t>(cuda_stream), h->d_counter);
 }
 
+eat_status eat_query_many_target_device(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times,
+                                        const uint32_t *d_dsts, uint64_t nq, uint32_t *d_out, void *cuda_stream) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
+    if (nq == 0) return EAT_OK;
+    if (!d_sources || !d_times || !d_dsts || !d_out) return fail(EAT_EINVAL, "NULL argument");
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
+        return fail(EAT_ESTATE, "batched queries need a replicated handle (query-parallel sharding)");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_TRY(cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (h->cta_grid > 0) {
+        CUDA_TRY(eat::launch_query_cta(h->ix, int(h->subwarp), d_sources, d_times, nq, d_out, nullptr, h->d_counter,
+                                       h->d_invalid, 0, h->d_work, st, d_dsts));
+        return EAT_OK;
+    }
+    // e[] too large for shared memory: full single queries, then e[dst]
+    std::vector<uint32_t> hs(nq), ht(nq), hd(nq);
+    CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sources, nq * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(ht.data(), d_times, nq * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(hd.data(), d_dsts, nq * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const uint32_t inf = EAT_INF;
+    for (uint64_t q = 0; q < nq; ++q) {
+        if (hs[q] >= h->hx.n || ht[q] >= EAT_INF || hd[q] >= h->hx.n) {
+            CUDA_TRY(cudaMemcpyAsync(d_out + q, &inf, 4, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            continue;
+        }
+        eat_status e = enqueue_single(h, hs[q], ht[q], h->d_out1, st);
+        if (e != EAT_OK) return e;
+        CUDA_TRY(cudaMemcpyAsync(d_out + q, h->d_out1 + hd[q], 4, cudaMemcpyDeviceToDevice, st));
+    }
+    return EAT_OK;
+}
+
+eat_status eat_query_many_target(eat_handle *h, const uint32_t *sources, const uint32_t *times, const uint32_t *dsts,
+                                 uint64_t nq, uint32_t *out) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
+    if (nq == 0) return EAT_OK;
+    if (!sources || !times || !dsts || !out) return fail(EAT_EINVAL, "NULL argument");
+    for (uint64_t q = 0; q < nq; ++q) {
+        if (sources[q] >= h->hx.n || dsts[q] >= h->hx.n)
+            return fail(EAT_EINVAL, "invalid source or destination vertex id at index " + std::to_string(q));
+        if (times[q] >= EAT_INF) return fail(EAT_ERANGE, "t_s >= EAT_INF at index " + std::to_string(q));
+    }
+    uint32_t *d = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(h->mu);
+        CUDA_TRY(cudaSetDevice(h->device));
+        CUDA_TRY(cudaMallocAsync(&d, nq * 16, h->stream));
+        CUDA_TRY(cudaMemcpyAsync(d, sources, nq * 4, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(cudaMemcpyAsync(d + nq, times, nq * 4, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(cudaMemcpyAsync(d + 2 * nq, dsts, nq * 4, cudaMemcpyHostToDevice, h->stream));
+    }
+    eat_status e = eat_query_many_target_device(h, d, d + nq, d + 2 * nq, nq, d + 3 * nq, h->stream);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (e == EAT_OK) {
+        CUDA_TRY(cudaMemcpyAsync(out, d + 3 * nq, nq * 4, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
+    cudaFreeAsync(d, h->stream);
+    return e;
+}
+
 eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t *times, uint64_t nq,
                           uint32_t *out) {
     if (!h) return fail(EAT_EINVAL, "NULL handle");

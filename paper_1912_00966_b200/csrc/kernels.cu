@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
                                                                uint32_t *__restrict__ out, uint32_t *sweeps_out,
                                                                unsigned long long *qcounter,
                                                                unsigned long long *invalid,
-                                                               unsigned long long *counters) {
+                                                               unsigned long long *counters,
+                                                               const uint32_t *__restrict__ dstv) {
     constexpr uint32_t kCtaWarps = kCtaThreads / 32;
     extern __shared__ uint32_t sm[];
     const uint32_t n = ix.n;
@@ -110,9 +111,15 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
         const unsigned long long q = s_q;
         if (q >= nq) break;
         const uint32_t s = src[q], ts = tsv[q];
-        uint32_t *orow = out + q * uint64_t(n);
-        if (s >= n || ts >= kInf) {
-            for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = kInf;
+        // goal-directed query (NEXT-4): only e[dst] is wanted
+        const uint32_t dq = dstv ? dstv[q] : 0u;
+        uint32_t *orow = dstv ? out + q : out + q * uint64_t(n);
+        if (s >= n || ts >= kInf || dq >= n) {
+            if (dstv) {
+                if (tid == 0) orow[0] = kInf;
+            } else {
+                for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = kInf;
+            }
             if (tid == 0) {
                 atomicAdd(invalid, 1ull);
                 if (sweeps_out) sweeps_out[q] = 0;
@@ -139,6 +146,7 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
             bmN[si >> 5] = 1u << (si & 31u);
         }
         __syncthreads();
+        const uint32_t di = dstv ? __ldg(ix.perm + dq) : 0u;
         uint32_t sweeps = 0;
         uint32_t c_vis = 0, c_type = 0, c_crec = 0, c_spill = 0, c_impr = 0;
         for (;;) {
@@ -149,21 +157,24 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
                 const uint32_t base = s_tmin[sweeps % 3u];
                 thr = base + min(window, kInf - base);  // saturating
             }
+            // goal-directed: a vertex with e[u] >= e[dst] cannot lower e[dst]
+            const uint32_t best = dstv ? uint32_t(varr[di]) : uint32_t(kInf);
             // ---- 1. select + compact: active = deferred | new
             uint32_t dmin = kInf, ndef = 0;
             for (uint32_t w = tid; w < W; w += kCtaThreads) {
-                const uint32_t word = bmD[w] | bmN[w];
+                uint32_t word = bmD[w] | bmN[w];
                 if (!word) continue;
                 bmN[w] = 0;
                 uint32_t sel = word;
-                if (thr < kInf) {
+                if (thr < kInf || best < kInf) {
                     sel = 0;
                     uint32_t rest = word;
                     while (rest) {
                         const uint32_t b = __ffs(rest) - 1u;
                         rest &= rest - 1u;
                         const uint32_t a = varr[w * 32u + b];
-                        if (a <= thr) sel |= 1u << b;
+                        if (a >= best) word &= ~(1u << b);  // pruned for good
+                        else if (a <= thr) sel |= 1u << b;
                         else dmin = min(dmin, a);
                     }
                 }
@@ -242,7 +253,8 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
                     if (COUNT) ++c_type;
                     if (eu > tr.last) continue;
                     const uint32_t av = varr[tr.v];
-                    if (max(eu, tr.first) + tr.lam >= av) continue;
+                    const uint32_t lim = dstv ? min(av, varr[di]) : av;
+                    if (max(eu, tr.first) + tr.lam >= lim) continue;  // PAPER.md:411-416 (+ target bound)
                     uint32_t tc;
                     if (eu <= tr.first) {
                         tc = tr.first;
@@ -273,7 +285,11 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
             if (s_more[p] == 0u) break;  // nothing deferred, nothing lowered: fixpoint
         }
         // Output in caller ids
-        for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = varr[__ldg(ix.perm + i)];
+        if (dstv) {
+            if (tid == 0) orow[0] = varr[di];
+        } else {
+            for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = varr[__ldg(ix.perm + i)];
+        }
         if (tid == 0 && sweeps_out) sweeps_out[q] = sweeps;
         if (COUNT) {
             unsigned long long v[5] = {c_vis, c_type, c_crec, c_spill, c_impr};
@@ -459,7 +475,7 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
 template <bool COUNT, int T, int L>
 cudaError_t launch_cta_sw(const DevIndex &ix, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
                           uint32_t *sweeps, unsigned long long *qc, unsigned long long *inv, int grid_cap,
-                          unsigned long long *counters, cudaStream_t st) {
+                          unsigned long long *counters, const uint32_t *dst, cudaStream_t st) {
     const size_t smem = cta_smem_bytes(ix.n);
     cudaError_t e = cudaFuncSetAttribute(k_query_cta<COUNT, T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
@@ -474,19 +490,19 @@ cudaError_t launch_cta_sw(const DevIndex &ix, const uint32_t *src, const uint32_
     if (grid == 0) return cudaSuccess;
     e = cudaMemsetAsync(qc, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    k_query_cta<COUNT, T, L><<<unsigned(grid), T, smem, st>>>(ix, src, ts, nq, out, sweeps, qc, inv, counters);
+    k_query_cta<COUNT, T, L><<<unsigned(grid), T, smem, st>>>(ix, src, ts, nq, out, sweeps, qc, inv, counters, dst);
     return cudaGetLastError();
 }
 
 template <bool COUNT>
 cudaError_t launch_cta_variant(int variant, const DevIndex &ix, const uint32_t *src, const uint32_t *ts, uint64_t nq,
                                uint32_t *out, uint32_t *sweeps, unsigned long long *qc, unsigned long long *inv,
-                               int grid_cap, unsigned long long *counters, cudaStream_t st) {
+                               int grid_cap, unsigned long long *counters, const uint32_t *dst, cudaStream_t st) {
     switch (variant) {
-        case 1024: return launch_cta_sw<COUNT, 1024, 2048>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
-        case 384: return launch_cta_sw<COUNT, 384, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
-        case 256: return launch_cta_sw<COUNT, 256, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
-        default: return launch_cta_sw<COUNT, 512, 2048>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, st);
+        case 1024: return launch_cta_sw<COUNT, 1024, 2048>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, dst, st);
+        case 384: return launch_cta_sw<COUNT, 384, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, dst, st);
+        case 256: return launch_cta_sw<COUNT, 256, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, dst, st);
+        default: return launch_cta_sw<COUNT, 512, 2048>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, dst, st);
     }
 }
 
@@ -558,12 +574,12 @@ cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint
 cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_src, const uint32_t *d_ts,
                              uint64_t nq, uint32_t *d_out, uint32_t *d_sweeps, unsigned long long *d_qcounter,
                              unsigned long long *d_invalid, int grid_cap, unsigned long long *d_counters,
-                             cudaStream_t st) {
+                             cudaStream_t st, const uint32_t *d_dst) {
     (void)subwarp;  // the CTA kernel flattens (vertex, type) pairs: no sub-warps
     return d_counters ? launch_cta_variant<true>(ix.cta_threads, ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter,
-                                                 d_invalid, grid_cap, d_counters, st)
+                                                 d_invalid, grid_cap, d_counters, d_dst, st)
                       : launch_cta_variant<false>(ix.cta_threads, ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter,
-                                                  d_invalid, grid_cap, nullptr, st);
+                                                  d_invalid, grid_cap, nullptr, d_dst, st);
 }
 
 cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,

@@ -42,10 +42,11 @@ cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint
 
 // One CTA per query, arr in shared memory.  d_qcounter: one uint64 zeroed here.
 // d_counters: NULL, or 6 uint64 work counters accumulated by the instrumented variant.
+// d_dst: NULL (d_out = [nq][n] rows), or per-query targets (d_out = [nq] arrival at the target, pruned search).
 cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_src, const uint32_t *d_ts,
                              uint64_t nq, uint32_t *d_out, uint32_t *d_sweeps, unsigned long long *d_qcounter,
                              unsigned long long *d_invalid, int grid_cap, unsigned long long *d_counters,
-                             cudaStream_t st);
+                             cudaStream_t st, const uint32_t *d_dst = nullptr);
 
 // Grid-wide persistent kernel for one query with global arr (cooperative launch).
 // subwarp 0: warp-flattened pairs + time window (default); 1..32: virtual warps of that width.

@@ -120,6 +120,22 @@ class Engine:
         _lib.eat_query_many(self._h, src.ctypes.data, ts.ctypes.data, src.shape[0], out.ctypes.data)
         return out
 
+    def query_targets(self, sources, times, dsts) -> np.ndarray:
+        """Goal-directed EAT (eat_query_many_target): arrival at dsts[i] per query."""
+        src, ts, dst = _u32(sources), _u32(times), _u32(dsts)
+        if not (src.shape == ts.shape == dst.shape):
+            raise ValueError("sources, times and dsts must have equal length")
+        out = np.empty(src.shape[0], dtype=np.uint32)
+        _lib.eat_query_many_target(self._h, src.ctypes.data, ts.ctypes.data, dst.ctypes.data, src.shape[0],
+                                   out.ctypes.data)
+        return out
+
+    def query_targets_device(self, sources, times, dsts, out, stream=None):
+        """int32 CUDA tensors [nq]; out [nq] receives the arrival at each target."""
+        _lib.eat_query_many_target_device(self._h, sources.data_ptr(), times.data_ptr(), dsts.data_ptr(),
+                                          int(sources.numel()), out.data_ptr(), _stream_ptr(stream))
+        return out
+
     def query_device(self, s: int, t_s: int, out, stream=None):
         """out: int32/uint32 CUDA tensor [num_vertices] on this engine's device."""
         _lib.eat_query_device(self._h, int(s), int(t_s), out.data_ptr(), _stream_ptr(stream))

@@ -284,6 +284,33 @@ def test_country_single_query():
         eng.close()
 
 
+def test_goal_directed_targets():
+    """NEXT-4: eat_query_many_target returns the oracle's e[dst] (pruned
+    search on the CTA kernel; full query + gather on the grid path)."""
+    for name, nq in (("tiny", 400), ("city", 300), ("metro", 6)):
+        tt = synth.generate(name)
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        rng = np.random.default_rng(17)
+        src, ts = synth.queries(tt, nq, 1, seed=3)
+        dst = rng.integers(0, tt.num_vertices, src.size).astype(np.uint32)
+        dst[::7] = src[::7]  # target == source
+        want = csa.query_many(src, ts)[np.arange(src.size), dst]
+        for kw in ({}, {"window": 0x7FFFFFFF}, {"subtrips": 2}):
+            eng = Engine.from_timetable(tt, **kw)
+            _assert_rows(eng.query_targets(src, ts, dst), want, f"targets {name} {kw}")
+            eng.close()
+    for seed in range(80):
+        tt = synth.random_small(5000 + seed)
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        eng = Engine.from_timetable(tt)
+        rng = np.random.default_rng(seed)
+        src = rng.integers(0, tt.num_vertices, 5).astype(np.uint32)
+        ts = rng.integers(0, 86400, 5).astype(np.uint32)
+        dst = rng.integers(0, tt.num_vertices, 5).astype(np.uint32)
+        want = csa.query_many(src, ts)[np.arange(5), dst]
+        _assert_rows(eng.query_targets(src, ts, dst), want, f"targets seed {seed}")
+
+
 @pytest.mark.parametrize("scheme", [1, 2])
 def test_subtrips_parity(scheme):
     """NEXT-1: the index with sub-trip shortcuts gives the oracle's arrival
