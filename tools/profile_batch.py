@@ -19,17 +19,18 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--single", default="")
 ap.add_argument("--subwarp", type=int, default=8)
 ap.add_argument("--window", type=int, default=0)
+ap.add_argument("--subtrips", type=int, default=2)
 a = ap.parse_args()
 tt = synth.generate(a.config)
 if a.single:
-    eng = Engine.from_timetable(tt, kernel=a.single, subwarp=a.subwarp, window=a.window)
+    eng = Engine.from_timetable(tt, kernel=a.single, subwarp=a.subwarp, window=a.window, subtrips=a.subtrips)
     out = torch.empty(tt.num_vertices, dtype=torch.int32, device="cuda")
     for _ in range(a.reps):
         eng.query_device(*synth.SINGLE_QUERY, out)
     torch.cuda.synchronize()
     print("sweeps", eng.stats()["last_sweeps"])
 else:
-    eng = Engine.from_timetable(tt, subwarp=a.subwarp, window=a.window)
+    eng = Engine.from_timetable(tt, subwarp=a.subwarp, window=a.window, subtrips=a.subtrips)
     src, ts = synth.queries(tt, a.nq // 10, 10)
     d_src = torch.tensor(src.astype(np.int32), device="cuda")
     d_ts = torch.tensor(ts.astype(np.int32), device="cuda")
