@@ -118,12 +118,19 @@ typedef struct eat_build_opts {
                                      e[u] <= min_active(e) + window (others stay active); EAT_INF = every
                                      active vertex (the paper's schedule); 0 -> EAT_DEFAULT_WINDOW.
                                      Results are identical for every value (same fixpoint). */
-    uint32_t cta_threads;         /* CTA kernel threads per query: 0 -> 256; 512, 384 or 256 (occupancy knob,
-                                     tools/sweep_cta.py) */
+    uint32_t cta_threads;         /* batched CTA kernel threads per query: 0 -> 256; 512, 384, 256, 192 or 128
+                                     (occupancy knob, tools/sweep_cta.py) */
     uint32_t subtrips;            /* sub-trip shortcuts (needs tt->trip): 0 off;
                                      1 = r = round(sqrt(k)) per trip of k connections;
                                      2 = r = round(sqrt(average trip length)); >= 3: r itself.
                                      Arrival times are unchanged; sweeps (hops) drop. */
+    uint32_t arr_bits;            /* batched CTA kernel e[] in shared memory: 0/16 -> uint16 offsets from t_s
+                                     (twice the queries per SM; a query whose arrivals pass t_s + 65534 s is
+                                     recomputed with uint32), 32 -> uint32 only.  Results identical. */
+    uint32_t cluster_dir;         /* cluster-record addressing: 0 auto (dense for |V| > 52k when it costs <= 3x),
+                                     1 dense (record of type t, cluster k at t*y + k -- the paper's CL[y*i+j],
+                                     PAPER.md:386-390: fetched in parallel with the type record),
+                                     2 compact (records only for [c_first, c_last] of each type) */
 } eat_build_opts;
 
 #define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */

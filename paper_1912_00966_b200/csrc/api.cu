@@ -74,7 +74,10 @@ struct eat_handle {
     uint32_t subwarp = 8;
     uint32_t mode = EAT_MODE_REPLICATED;
     uint32_t window = EAT_INF;           // CTA schedule time window (EAT_INF = all active vertices)
-    uint32_t cta_threads = 512;          // CTA-kernel variant
+    uint32_t cta_threads = 256;          // CTA-kernel variant (batched queries)
+    bool arr16 = true;                   // batched CTA kernel keeps e[] as uint16 offsets (+ uint32 recompute)
+    uint32_t *d_ovf[3] = {nullptr, nullptr, nullptr};  // overflow lists: device API, pipeline stages 0/1
+    uint64_t ovf_cap[3] = {0, 0, 0};
     cudaStream_t stream = nullptr;
     // device index: slices[0] is this handle's index (whole, or its own edge
     // partition); a loopback edge-partitioned handle holds all P partitions
@@ -114,7 +117,7 @@ void release_device(eat_handle *h) {
     void *ptrs[] = {h->d_perm,  h->gw.arr, h->gw.q0,     h->gw.q1,      h->gw.stamp,   h->gw.bm,
                     h->gw.ctl,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
                     h->d_bsrc[0], h->d_bts[0], h->d_bout[0], h->d_bsrc[1], h->d_bts[1], h->d_bout[1],
-                    h->d_bcounter, h->d_work, h->d_rounds1};
+                    h->d_bcounter, h->d_work, h->d_rounds1, h->d_ovf[0], h->d_ovf[1], h->d_ovf[2]};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     eat::async_free(h->aw);
@@ -179,6 +182,7 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     CUDA_TRY(dalloc_copy(&sl.type_src, tsrc.data(), tsrc.size(), b));
     sl.ix.n = n;
     sl.ix.cs = x.cs;
+    sl.ix.dense_nc = x.dense_nc;
     {
         uint32_t l = 0;
         while ((1u << l) < x.cs) ++l;  // ceil(log2 cs)
@@ -275,7 +279,7 @@ eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_
 }
 
 eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
-    h->cta_grid = eat::cta_grid_size(h->hx.n, int(h->ix.cta_threads));
+    h->cta_grid = eat::cta_grid_size(h->hx.n, int(h->cta_threads), h->arr16);
     h->st.smem_vertices_max = 0;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
@@ -318,11 +322,19 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
     if (h->kernel == EAT_KERNEL_CTA) {
         uint32_t q[2] = {s, t_s};
         CUDA_TRY(cudaMemcpyAsync(h->d_q1, q, sizeof(q), cudaMemcpyHostToDevice, st));
-        // a lone query gets the widest CTA (1024 threads): it has the SM to itself
-        eat::DevIndex ix1 = h->ix;
-        ix1.cta_threads = 1024;
-        CUDA_TRY(eat::launch_query_cta(ix1, int(h->subwarp), h->d_q1, h->d_q1 + 1, 1, d_out, h->d_sweeps1,
-                                       h->d_counter, h->d_invalid, 1, nullptr, st));
+        // a lone query gets the widest CTA (1024 threads, uint32 e[]): it has the SM to itself
+        eat::CtaArgs a;
+        a.src = h->d_q1;
+        a.ts = h->d_q1 + 1;
+        a.nq = 1;
+        a.out = d_out;
+        a.sweeps = h->d_sweeps1;
+        a.qcounter = h->d_counter;
+        a.invalid = h->d_invalid;
+        a.threads = 1024;
+        a.arr16 = false;
+        a.grid_cap = 1;
+        CUDA_TRY(eat::launch_query_cta(h->ix, a, st));
     } else if (h->kernel == EAT_KERNEL_ASYNC) {
         CUDA_TRY(eat::launch_query_async(h->ix, h->aw, s, t_s, d_out, st));
         CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->aw.ctl + 9, 4, cudaMemcpyDeviceToDevice, st));
@@ -350,6 +362,8 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     eat::BuildParams p;
     p.cs = o.cluster_seconds ? o.cluster_seconds : 3600;
     p.renumber = o.renumber;
+    if (o.cluster_dir > 2) return fail(EAT_EINVAL, "cluster_dir must be 0 (auto), 1 (dense) or 2 (compact)");
+    p.dense = o.cluster_dir;
     const uint32_t sw = o.subwarp == 0 ? 32u : (o.subwarp == 64 ? 0u : o.subwarp);  // 0 internally = flattened
     if (sw != 0 && sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
         return fail(EAT_EINVAL, "subwarp must be 0 (default 32), 1, 2, 4, 8, 16, 32 or 64 (flattened pairs)");
@@ -364,10 +378,16 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     h->mode = o.mode;
     h->window = o.window_seconds == 0 ? EAT_DEFAULT_WINDOW : o.window_seconds;
     h->cta_threads = o.cta_threads == 0 ? 256u : o.cta_threads;
-    if (h->cta_threads != 512 && h->cta_threads != 384 && h->cta_threads != 256) {
+    if (h->cta_threads != 512 && h->cta_threads != 384 && h->cta_threads != 256 && h->cta_threads != 192 &&
+        h->cta_threads != 128) {
         delete h;
-        return fail(EAT_EINVAL, "cta_threads must be 256, 384 or 512");
+        return fail(EAT_EINVAL, "cta_threads must be 128, 192, 256, 384 or 512");
     }
+    if (o.arr_bits != 0 && o.arr_bits != 16 && o.arr_bits != 32) {
+        delete h;
+        return fail(EAT_EINVAL, "arr_bits must be 0, 16 or 32");
+    }
+    h->arr16 = o.arr_bits == 16;  // default uint32 (tools/sweep_cta.py: uint16 gives no gain)
     h->part_rank = o.part_rank;
     h->part_count = pc;
     h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 && !o.nccl_unique_id;
@@ -540,13 +560,43 @@ namespace {
 
 // Enqueue a batch of device-resident queries on st (CTA kernel), or, when e[]
 // does not fit shared memory, one single-query launch after another.
-eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
-                         uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter) {
-    if (h->cta_grid > 0) {
-        CUDA_TRY(eat::launch_query_cta(h->ix, int(h->subwarp), d_sources, d_times, nq, d_out, nullptr, d_qcounter,
-                                       h->d_invalid, 0, h->d_work, st));
-        return EAT_OK;
+// Launch the batched CTA kernel (uint16 pass + uint32 recompute of overflows);
+// `slot` selects the overflow list (0: device API, 1/2: pipeline stages).
+eat_status launch_batch_cta(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
+                            uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, int slot,
+                            const uint32_t *d_dst) {
+    if (h->arr16 && h->ovf_cap[slot] < nq + 1) {
+        if (h->d_ovf[slot]) {
+            CUDA_TRY(cudaStreamSynchronize(st));
+            cudaFree(h->d_ovf[slot]);
+        }
+        h->d_ovf[slot] = nullptr;
+        h->ovf_cap[slot] = 0;
+        CUDA_TRY(cudaMalloc(&h->d_ovf[slot], (nq + 1) * 4));
+        h->ovf_cap[slot] = nq + 1;
     }
+    eat::CtaArgs a;
+    a.src = d_sources;
+    a.ts = d_times;
+    a.nq = nq;
+    a.out = d_out;
+    a.qcounter = d_qcounter;
+    a.invalid = h->d_invalid;
+    a.counters = h->d_work;
+    a.dst = d_dst;
+    a.threads = int(h->cta_threads);
+    a.arr16 = h->arr16;
+    if (h->arr16) {
+        a.ovf_list = h->d_ovf[slot] + 1;
+        a.ovf_cnt = h->d_ovf[slot];
+    }
+    CUDA_TRY(eat::launch_query_cta(h->ix, a, st));
+    return EAT_OK;
+}
+
+eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
+                         uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, int slot = 0) {
+    if (h->cta_grid > 0) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, d_qcounter, slot, nullptr);
     std::vector<uint32_t> hs(nq), ht(nq);
     CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sources, nq * 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(ht.data(), d_times, nq * 4, cudaMemcpyDeviceToHost, st));
@@ -609,11 +659,7 @@ eat_status eat_query_many_target_device(eat_handle *h, const uint32_t *d_sources
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_TRY(cudaSetDevice(h->device));
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    if (h->cta_grid > 0) {
-        CUDA_TRY(eat::launch_query_cta(h->ix, int(h->subwarp), d_sources, d_times, nq, d_out, nullptr, h->d_counter,
-                                       h->d_invalid, 0, h->d_work, st, d_dsts));
-        return EAT_OK;
-    }
+    if (h->cta_grid > 0) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, h->d_counter, 0, d_dsts);
     // e[] too large for shared memory: full single queries, then e[dst]
     std::vector<uint32_t> hs(nq), ht(nq), hd(nq);
     CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sources, nq * 4, cudaMemcpyDeviceToHost, st));
@@ -723,7 +769,7 @@ eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t
             cudaStream_t st = h->bstream[b];
             CUDA_TRY(cudaMemcpyAsync(h->d_bsrc[b], sources + q0, c * 4, cudaMemcpyHostToDevice, st));
             CUDA_TRY(cudaMemcpyAsync(h->d_bts[b], times + q0, c * 4, cudaMemcpyHostToDevice, st));
-            eat_status e = enqueue_batch(h, h->d_bsrc[b], h->d_bts[b], c, h->d_bout[b], st, h->d_bcounter + b);
+            eat_status e = enqueue_batch(h, h->d_bsrc[b], h->d_bts[b], c, h->d_bout[b], st, h->d_bcounter + b, 1 + b);
             if (e != EAT_OK) return e;
             CUDA_TRY(cudaMemcpyAsync(pinned ? out + q0 * n : h->h_stage[b], h->d_bout[b], c * n * 4,
                                      cudaMemcpyDeviceToHost, st));

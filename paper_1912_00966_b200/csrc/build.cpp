@@ -526,6 +526,37 @@ int build_host_index(uint32_t n, uint64_t m, const uint32_t *u, const uint32_t *
         std::vector<uint32_t>().swap(ch.pool);
     }
     ix.num_crec = R;
+    // 8. dense cluster directory (the paper's CL[y*i + j] addressing,
+    // PAPER.md:386-390): record of (type t, cluster k) at t*NC + k, so a
+    // kernel can fetch it from (t, e[u]) alone, in parallel with the type
+    // record -- one dependent load less per relaxation.  Used when it costs at
+    // most ~3x the compact layout; records outside [c_first, c_last] are never
+    // read (the lookup only reaches a cluster record when first < e[u] <= last).
+    const uint64_t NC = uint64_t(ix.max_dep) / cs + 1;
+    const uint64_t dense_recs = T * NC;
+    bool dense = p.dense == 1;
+    // auto: only graphs too large for the shared-memory (CTA) kernels, which
+    // run the latency-bound grid kernels (measured: metro -5 %, city batch +14 %
+    // slower with dense because of the speculative record loads)
+    if (p.dense == 0)
+        dense = n > 52000 && dense_recs * kCrecWords * 4 <= 3 * R * kCrecWords * 4;
+    if (dense && T && dense_recs < 0xFFFFFFF0ull) {
+        std::vector<uint32_t> dcrec(dense_recs * kCrecWords, 0u);
+        parallel_chunks(T, [&](uint64_t lo, uint64_t hi) {
+            for (uint64_t t = lo; t < hi; ++t) {
+                uint32_t *tr = ix.type_rec.data() + t * kTypeWords;
+                const uint32_t cf = tr[5], cl = tr[3] / cs;
+                std::copy(ix.crec.begin() + uint64_t(tr[4]) * kCrecWords,
+                          ix.crec.begin() + (uint64_t(tr[4]) + (cl - cf + 1)) * kCrecWords,
+                          dcrec.begin() + (t * NC + cf) * kCrecWords);
+                tr[4] = uint32_t(t * NC);  // crec_base
+                tr[5] = 0;                 // c_first: record index = crec_base + k
+            }
+        });
+        ix.crec.swap(dcrec);
+        ix.num_crec = dense_recs;
+        ix.dense_nc = uint32_t(NC);
+    }
     ix.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return EAT_OK;
 }

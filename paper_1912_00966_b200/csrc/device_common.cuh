@@ -42,15 +42,12 @@ __device__ __forceinline__ uint32_t cluster_of(const DevIndex &ix, uint32_t e) {
     return uint32_t((uint64_t(e) * ix.cs_magic) >> ix.cs_shift);
 }
 
-// Cluster-AP lookup inside the type's cluster k = eu / cs:
-// smallest term >= eu among the cluster's APs, else the first departure of
-// the next non-empty cluster (precomputed as next_min).
-// Precondition: first < eu <= last (so c_first <= k <= c_last).
-__device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t crec_base, uint32_t c_first,
-                                                   uint32_t eu) {
-    const uint32_t k = cluster_of(ix, eu);
-    const uint32_t r = crec_base + (k - c_first);
-    const uint4 r0 = __ldg(ix.crec + 2ull * r);
+// Cluster-AP lookup inside the type's cluster k = eu / cs,
+// given the cluster's 32-byte record (r0, r1): smallest term >= eu among the
+// cluster's APs, else the first departure of the next non-empty cluster
+// (precomputed as next_min).  Precondition: first < eu <= last.
+__device__ __forceinline__ uint32_t cluster_scan(const DevIndex &ix, const uint4 &r0, const uint4 &r1, uint32_t k,
+                                                 uint32_t eu) {
     const uint32_t x = eu - k * ix.cs;
     uint32_t best = kNone;
     if (r0.y == kItemSpill) {
@@ -60,7 +57,6 @@ __device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t 
             if ((it & 0xFFFu) >= x) break;  // items sorted by first term: later ones start later
         }
     } else {
-        const uint4 r1 = __ldg(ix.crec + 2ull * r + 1);
         const uint32_t items[kInlineItems] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
         for (int i = 0; i < kInlineItems; ++i) {
@@ -70,6 +66,33 @@ __device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t 
         }
     }
     return best != kNone ? k * ix.cs + best : r0.x;
+}
+
+__device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t crec_base, uint32_t c_first,
+                                                   uint32_t eu) {
+    const uint32_t k = cluster_of(ix, eu);
+    const uint64_t r = uint64_t(crec_base) + (k - c_first);
+    const uint4 r0 = __ldg(ix.crec + 2 * r);
+    const uint4 r1 = __ldg(ix.crec + 2 * r + 1);
+    return cluster_scan(ix, r0, r1, k, eu);
+}
+
+// Dense cluster directory (ix.dense_nc > 0): the record of (type t, cluster
+// of eu) has a computable address, so it is fetched together with the type
+// record instead of after it.  Out-of-range clusters are clamped (the value
+// is then unused: the lookup only reads it when first < eu <= last).
+struct CrecPrefetch {
+    uint4 r0, r1;
+    uint32_t k;
+};
+
+__device__ __forceinline__ CrecPrefetch crec_prefetch(const DevIndex &ix, uint64_t t, uint32_t eu) {
+    CrecPrefetch p;
+    p.k = cluster_of(ix, eu);
+    const uint64_t r = t * ix.dense_nc + min(p.k, ix.dense_nc - 1u);
+    p.r0 = __ldg(ix.crec + 2 * r);
+    p.r1 = __ldg(ix.crec + 2 * r + 1);
+    return p;
 }
 
 struct TypeRec {
@@ -125,11 +148,15 @@ __device__ __forceinline__ void push_aggregated(uint32_t v, uint32_t *q, uint32_
 // arrival eu, against a global e[] (atomicMin).  Returns
 // the target v when this call strictly lowered e[v], else kNone.
 __device__ __forceinline__ uint32_t relax_type_global(const DevIndex &ix, uint64_t t, uint32_t eu, uint32_t *arr) {
+    CrecPrefetch pf{};
+    if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);
     const TypeRec tr = load_type(ix, t);
     if (eu > tr.last) return kNone;
     const uint32_t av = __ldcg(arr + tr.v);
     if (max(eu, tr.first) + tr.lam >= av) return kNone;  // early termination
-    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+    const uint32_t tc = eu <= tr.first ? tr.first
+                                       : (ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
+                                                      : cluster_lookup(ix, tr.crec_base, tr.c_first, eu));
     const uint32_t cand = tc + tr.lam;
     if (cand >= av) return kNone;
     const uint32_t old = atomicMin(arr + tr.v, cand);

@@ -67,12 +67,14 @@ struct HostIndex {
     std::vector<uint32_t> crec;      // 8 * R
     std::vector<uint32_t> pool;      // spilled items
     uint64_t num_types = 0, num_edges = 0, num_crec = 0, num_items = 0;
+    uint32_t dense_nc = 0;           // > 0: dense cluster directory, record (t, k) at t*dense_nc + k
     double build_ms = 0.0;
 };
 
 struct BuildParams {
     uint32_t cs = 3600;
     uint32_t renumber = 0;
+    uint32_t dense = 0;   // cluster directory: 0 auto, 1 dense, 2 compact
 };
 
 struct SubtripStats {

@@ -76,46 +76,107 @@ __global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *boun
 // the work counters used for algorithmic-byte accounting:
 // counters[0] vertex visits, [1] type records read, [2] cluster records read,
 // [3] spilled items read, [4] improvements (successful atomicMin), [5] sweeps.
+// Shared-memory e[] of one query.  SArr<false>: uint32 arrival times.
+// SArr<true>: uint16 offsets from t_s (0xFFFF = unreached), half the shared
+// memory per query so more queries fit per SM; an improvement whose offset
+// would not fit (>= 18.2 h after t_s) raises the overflow flag and the query is
+// recomputed by the uint32 variant (exact either way).
+template <bool A16>
+struct SArr;
+
+template <>
+struct SArr<false> {
+    uint32_t *a;
+    uint32_t base;
+    __device__ __forceinline__ uint32_t get(uint32_t i) const { return reinterpret_cast<volatile uint32_t *>(a)[i]; }
+    __device__ __forceinline__ void init(uint32_t i) { a[i] = kInf; }
+    __device__ __forceinline__ void set(uint32_t i, uint32_t v) { a[i] = v; }
+    __device__ __forceinline__ uint32_t amin(uint32_t i, uint32_t v, uint32_t *) { return atomicMin(a + i, v); }
+    static __host__ __device__ size_t bytes(uint32_t n) { return size_t((n + 3u) & ~3u) * 4u; }
+};
+
+template <>
+struct SArr<true> {
+    uint16_t *a;
+    uint32_t base;
+    __device__ __forceinline__ uint32_t get(uint32_t i) const {
+        const uint32_t r = reinterpret_cast<volatile uint16_t *>(a)[i];
+        return r == 0xFFFFu ? kInf : base + r;
+    }
+    __device__ __forceinline__ void init(uint32_t i) { a[i] = 0xFFFFu; }
+    __device__ __forceinline__ void set(uint32_t i, uint32_t v) { a[i] = uint16_t(v - base); }
+    // atomic min on a 16-bit slot via 32-bit CAS on its word; returns the old arrival
+    __device__ __forceinline__ uint32_t amin(uint32_t i, uint32_t v, uint32_t *ovf) {
+        const uint32_t rel = v - base;
+        if (rel >= 0xFFFFu) {  // offset does not fit: recompute this query in uint32
+            *ovf = 1u;
+            return v;
+        }
+        uint32_t *w = reinterpret_cast<uint32_t *>(a) + (i >> 1);
+        const uint32_t sh = (i & 1u) * 16u;
+        uint32_t old = *reinterpret_cast<volatile uint32_t *>(w);
+        for (;;) {
+            const uint32_t cur = (old >> sh) & 0xFFFFu;
+            if (rel >= cur) return cur == 0xFFFFu ? kInf : base + cur;
+            const uint32_t nw = (old & ~(0xFFFFu << sh)) | (rel << sh);
+            const uint32_t prev = atomicCAS(w, old, nw);
+            if (prev == old) return cur == 0xFFFFu ? kInf : base + cur;
+            old = prev;
+        }
+    }
+    static __host__ __device__ size_t bytes(uint32_t n) { return size_t((n + 7u) & ~7u) * 2u; }
+};
+
 // Minimum resident CTAs per SM for the register budget: shared memory (e[]
 // of a 10k-stop city) already caps residency at 4 (512 threads) or 5.
-template <int T>
-constexpr int cta_min_blocks() { return T >= 1024 ? 1 : (T >= 512 ? 4 : 5); }
+template <int T, bool A16>
+constexpr int cta_min_blocks() { return T >= 1024 ? 1 : (A16 ? 8 : (T >= 512 ? 4 : 5)); }
 
-template <bool COUNT, int kCtaThreads, int kListCap>
-__global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
+template <bool COUNT, int kCtaThreads, int kListCap, bool A16, bool TGT>
+__global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>())) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
                                                                const uint32_t *__restrict__ tsv, uint64_t nq,
                                                                uint32_t *__restrict__ out, uint32_t *sweeps_out,
                                                                unsigned long long *qcounter,
                                                                unsigned long long *invalid,
                                                                unsigned long long *counters,
-                                                               const uint32_t *__restrict__ dstv) {
+                                                               const uint32_t *__restrict__ dstv,
+                                                               const uint32_t *__restrict__ qlist,
+                                                               const uint32_t *__restrict__ qcount,
+                                                               uint32_t *__restrict__ ovf_list,
+                                                               uint32_t *__restrict__ ovf_cnt) {
     constexpr uint32_t kCtaWarps = kCtaThreads / 32;
     extern __shared__ uint32_t sm[];
     const uint32_t n = ix.n;
     const uint32_t W = (n + 31u) / 32u;
     const uint32_t npad = (n + 3u) & ~3u;
-    uint32_t *arr = sm;
-    volatile uint32_t *varr = sm;
-    uint32_t *bmD = sm + npad;  // deferred: active, not yet selected
+    SArr<A16> ar;
+    ar.a = reinterpret_cast<decltype(ar.a)>(sm);
+    uint32_t *bmD = sm + SArr<A16>::bytes(n) / 4u;  // deferred: active, not yet selected
     uint32_t *bmN = bmD + W;    // new: lowered since their last selection
     __shared__ uint32_t s_list[kListCap];
     __shared__ uint32_t s_cnt[2], s_more[2];  // per sweep parity: listed / (deferred + improved)
     __shared__ uint32_t s_tmin[3];            // window base, rotating per sweep
+    __shared__ uint32_t s_ovf;                // A16: an arrival offset overflowed
     __shared__ unsigned long long s_q;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
     const uint32_t window = ix.window;
+    (void)npad;
+    const uint64_t nq_eff = qcount ? uint64_t(*qcount) : nq;
 
     for (;;) {
-        if (tid == 0) s_q = atomicAdd(qcounter, 1ull);
+        if (tid == 0) {
+            const unsigned long long qi = atomicAdd(qcounter, 1ull);
+            s_q = qi >= nq_eff ? ~0ull : (qlist ? (unsigned long long)qlist[qi] : qi);
+        }
         __syncthreads();
         const unsigned long long q = s_q;
-        if (q >= nq) break;
+        if (q == ~0ull) break;
         const uint32_t s = src[q], ts = tsv[q];
         // goal-directed query (NEXT-4): only e[dst] is wanted
-        const uint32_t dq = dstv ? dstv[q] : 0u;
-        uint32_t *orow = dstv ? out + q : out + q * uint64_t(n);
+        const uint32_t dq = TGT ? dstv[q] : 0u;
+        uint32_t *orow = TGT ? out + q : out + q * uint64_t(n);
         if (s >= n || ts >= kInf || dq >= n) {
-            if (dstv) {
+            if (TGT) {
                 if (tid == 0) orow[0] = kInf;
             } else {
                 for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = kInf;
@@ -128,7 +189,8 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
             continue;
         }
         // Initialize (Algorithm 2)
-        for (uint32_t i = tid; i < n; i += kCtaThreads) arr[i] = kInf;
+        ar.base = ts;
+        for (uint32_t i = tid; i < n; i += kCtaThreads) ar.init(i);
         for (uint32_t i = tid; i < W; i += kCtaThreads) {
             bmD[i] = 0;
             bmN[i] = 0;
@@ -138,15 +200,16 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
             s_more[0] = s_more[1] = 0;
             s_tmin[0] = ts;
             s_tmin[1] = s_tmin[2] = kInf;
+            s_ovf = 0;
         }
         __syncthreads();
         if (tid == 0) {
             const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
-            arr[si] = ts;
+            ar.set(si, ts);
             bmN[si >> 5] = 1u << (si & 31u);
         }
         __syncthreads();
-        const uint32_t di = dstv ? __ldg(ix.perm + dq) : 0u;
+        const uint32_t di = TGT ? __ldg(ix.perm + dq) : 0u;
         uint32_t sweeps = 0;
         uint32_t c_vis = 0, c_type = 0, c_crec = 0, c_spill = 0, c_impr = 0;
         for (;;) {
@@ -158,7 +221,7 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
                 thr = base + min(window, kInf - base);  // saturating
             }
             // goal-directed: a vertex with e[u] >= e[dst] cannot lower e[dst]
-            const uint32_t best = dstv ? uint32_t(varr[di]) : uint32_t(kInf);
+            const uint32_t best = TGT ? ar.get(di) : uint32_t(kInf);
             // ---- 1. select + compact: active = deferred | new
             uint32_t dmin = kInf, ndef = 0;
             for (uint32_t w = tid; w < W; w += kCtaThreads) {
@@ -166,14 +229,14 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
                 if (!word) continue;
                 bmN[w] = 0;
                 uint32_t sel = word;
-                if (thr < kInf || best < kInf) {
+                if (thr < kInf || (TGT && best < kInf)) {
                     sel = 0;
                     uint32_t rest = word;
                     while (rest) {
                         const uint32_t b = __ffs(rest) - 1u;
                         rest &= rest - 1u;
-                        const uint32_t a = varr[w * 32u + b];
-                        if (a >= best) word &= ~(1u << b);  // pruned for good
+                        const uint32_t a = ar.get(w * 32u + b);
+                        if (TGT && a >= best) word &= ~(1u << b);  // pruned for good
                         else if (a <= thr) sel |= 1u << b;
                         else dmin = min(dmin, a);
                     }
@@ -193,7 +256,7 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
                     while (rest) {  // list full: stays active for a later sweep
                         const uint32_t b = __ffs(rest) - 1u;
                         rest &= rest - 1u;
-                        dmin = min(dmin, varr[w * 32u + b]);
+                        dmin = min(dmin, ar.get(w * 32u + b));
                     }
                 }
                 bmD[w] = word & ~taken;
@@ -248,18 +311,21 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
                     const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
                     if (qp >= tot) continue;
                     const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
-                    const uint32_t eu = varr[u];
+                    const uint32_t eu = ar.get(u);
+                    CrecPrefetch pf{};
+                    if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the type record
                     const TypeRec tr = load_type(ix, t);
                     if (COUNT) ++c_type;
                     if (eu > tr.last) continue;
-                    const uint32_t av = varr[tr.v];
-                    const uint32_t lim = dstv ? min(av, varr[di]) : av;
+                    const uint32_t av = ar.get(tr.v);
+                    const uint32_t lim = TGT ? min(av, ar.get(di)) : av;
                     if (max(eu, tr.first) + tr.lam >= lim) continue;  // PAPER.md:411-416 (+ target bound)
                     uint32_t tc;
                     if (eu <= tr.first) {
                         tc = tr.first;
                     } else {
-                        tc = cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                        tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
+                                         : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
                         if (COUNT) {
                             ++c_crec;
                             const uint4 rr = __ldg(ix.crec + 2ull * (tr.crec_base + cluster_of(ix, eu) - tr.c_first));
@@ -268,7 +334,7 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
                     }
                     const uint32_t cand = tc + tr.lam;
                     if (cand < av) {
-                        const uint32_t old = atomicMin(arr + tr.v, cand);
+                        const uint32_t old = ar.amin(tr.v, cand, &s_ovf);
                         if (cand < old) {
                             atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
                             if (window < kInf) atomicMin(&s_tmin[t_nxt], cand);
@@ -283,12 +349,18 @@ __global__ void __launch_bounds__(kCtaThreads, cta_min_blocks<kCtaThreads>()) k_
             __syncthreads();
             ++sweeps;
             if (s_more[p] == 0u) break;  // nothing deferred, nothing lowered: fixpoint
+            if (A16 && s_ovf) break;      // recomputed by the uint32 variant
+        }
+        if (A16 && s_ovf) {
+            if (tid == 0) ovf_list[atomicAdd(ovf_cnt, 1u)] = uint32_t(q);
+            __syncthreads();
+            continue;
         }
         // Output in caller ids
-        if (dstv) {
-            if (tid == 0) orow[0] = varr[di];
+        if (TGT) {
+            if (tid == 0) orow[0] = ar.get(di);
         } else {
-            for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = varr[__ldg(ix.perm + i)];
+            for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = ar.get(__ldg(ix.perm + i));
         }
         if (tid == 0 && sweeps_out) sweeps_out[q] = sweeps;
         if (COUNT) {
@@ -425,17 +497,9 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
                 const uint32_t eu = ld_cg(w.arr + x);
                 const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
                 for (uint32_t t = p0 + lane; t < p1; t += SW) {
-                    const TypeRec tr = load_type(ix, t);
-                    if (eu > tr.last) continue;
-                    const uint32_t av = ld_cg(w.arr + tr.v);
-                    if (max(eu, tr.first) + tr.lam >= av) continue;
-                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
-                    const uint32_t cand = tc + tr.lam;
-                    if (cand < av) {
-                        const uint32_t old = atomicMin(w.arr + tr.v, cand);
-                        if (cand < old && atomicExch(w.stamp + tr.v, sweep + 1u) != sweep + 1u)
-                            push_aggregated(tr.v, qn, w.ctl + c_nxt);
-                    }
+                    const uint32_t v = relax_type_global(ix, t, eu, w.arr);
+                    if (v != kNone && atomicExch(w.stamp + v, sweep + 1u) != sweep + 1u)
+                        push_aggregated(v, qn, w.ctl + c_nxt);
                 }
             }
         } else {
@@ -472,37 +536,57 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     if (gtid == 0) w.ctl[8] = sweep;
 }
 
-template <bool COUNT, int T, int L>
-cudaError_t launch_cta_sw(const DevIndex &ix, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
-                          uint32_t *sweeps, unsigned long long *qc, unsigned long long *inv, int grid_cap,
-                          unsigned long long *counters, const uint32_t *dst, cudaStream_t st) {
-    const size_t smem = cta_smem_bytes(ix.n);
-    cudaError_t e = cudaFuncSetAttribute(k_query_cta<COUNT, T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+template <bool COUNT, int T, int L, bool A16, bool TGT = false>
+cudaError_t launch_cta_one(const DevIndex &ix, const CtaArgs &a, const uint32_t *qlist, const uint32_t *qcount,
+                           uint32_t *ovf_list, uint32_t *ovf_cnt, uint64_t grid_cap, cudaStream_t st) {
+    const size_t smem = cta_smem_bytes(ix.n, A16);
+    auto kern = k_query_cta<COUNT, T, L, A16, TGT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<COUNT, T, L>, T, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    uint64_t grid = std::min<uint64_t>(uint64_t(sms) * per_sm, nq);
-    if (grid_cap > 0) grid = std::min<uint64_t>(grid, uint64_t(grid_cap));
+    uint64_t grid = std::min<uint64_t>(uint64_t(sms) * per_sm, a.nq);
+    if (grid_cap > 0) grid = std::min<uint64_t>(grid, grid_cap);
     if (grid == 0) return cudaSuccess;
-    e = cudaMemsetAsync(qc, 0, sizeof(unsigned long long), st);
+    e = cudaMemsetAsync(a.qcounter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    k_query_cta<COUNT, T, L><<<unsigned(grid), T, smem, st>>>(ix, src, ts, nq, out, sweeps, qc, inv, counters, dst);
+    kern<<<unsigned(grid), T, smem, st>>>(ix, a.src, a.ts, a.nq, a.out, a.sweeps, a.qcounter, a.invalid, a.counters,
+                                          a.dst, qlist, qcount, ovf_list, ovf_cnt);
     return cudaGetLastError();
 }
 
+// uint16 pass over all queries, then the uint32 variant over the overflow
+// list (count read on the device; empty in practice for one-day feeds).
+template <bool COUNT, int T, int L>
+cudaError_t launch_cta_pair(const DevIndex &ix, const CtaArgs &a, cudaStream_t st) {
+    if (!a.arr16) return launch_cta_one<COUNT, T, L, false>(ix, a, nullptr, nullptr, nullptr, nullptr, a.grid_cap, st);
+    cudaError_t e = cudaMemsetAsync(a.ovf_cnt, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    e = launch_cta_one<COUNT, T, L, true>(ix, a, nullptr, nullptr, a.ovf_list, a.ovf_cnt, a.grid_cap, st);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return launch_cta_one<COUNT, T, L, false>(ix, a, a.ovf_list, a.ovf_cnt, nullptr, nullptr, uint64_t(sms), st);
+}
+
 template <bool COUNT>
-cudaError_t launch_cta_variant(int variant, const DevIndex &ix, const uint32_t *src, const uint32_t *ts, uint64_t nq,
-                               uint32_t *out, uint32_t *sweeps, unsigned long long *qc, unsigned long long *inv,
-                               int grid_cap, unsigned long long *counters, const uint32_t *dst, cudaStream_t st) {
-    switch (variant) {
-        case 1024: return launch_cta_sw<COUNT, 1024, 2048>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, dst, st);
-        case 384: return launch_cta_sw<COUNT, 384, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, dst, st);
-        case 256: return launch_cta_sw<COUNT, 256, 512>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, dst, st);
-        default: return launch_cta_sw<COUNT, 512, 2048>(ix, src, ts, nq, out, sweeps, qc, inv, grid_cap, counters, dst, st);
+cudaError_t launch_cta_variant(const DevIndex &ix, const CtaArgs &a, cudaStream_t st) {
+    if (a.dst) {  // goal-directed queries: one variant (256 threads, uint32 e[])
+        if (COUNT) return cudaErrorNotSupported;
+        return launch_cta_one<false, 256, 512, false, true>(ix, a, nullptr, nullptr, nullptr, nullptr, a.grid_cap, st);
+    }
+    switch (a.threads) {
+        case 1024: return launch_cta_pair<COUNT, 1024, 2048>(ix, a, st);
+        case 512: return launch_cta_pair<COUNT, 512, 2048>(ix, a, st);
+        case 384: return launch_cta_pair<COUNT, 384, 512>(ix, a, st);
+        case 192: return launch_cta_pair<COUNT, 192, 512>(ix, a, st);
+        case 128: return launch_cta_pair<COUNT, 128, 512>(ix, a, st);
+        default: return launch_cta_pair<COUNT, 256, 512>(ix, a, st);
     }
 }
 
@@ -527,39 +611,49 @@ cudaError_t launch_grid_sw(const DevIndex &ix, const GridWork &w, uint32_t s, ui
 
 }  // namespace
 
-size_t cta_smem_bytes(uint32_t n) {
-    const size_t npad = (n + 3u) & ~3u, W = (n + 31u) / 32u;
-    return (npad + 2 * W) * sizeof(uint32_t);
+size_t cta_smem_bytes(uint32_t n, bool a16) {
+    const size_t W = (n + 31u) / 32u;
+    return (a16 ? SArr<true>::bytes(n) : SArr<false>::bytes(n)) + 2 * W * sizeof(uint32_t);
 }
 
-template <int T, int L>
+template <int T, int L, bool A16>
 int cta_grid_size_t(uint32_t n) {
     int dev = 0, optin = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, k_query_cta<false, T, L>) != cudaSuccess) return 0;
-    const size_t need = cta_smem_bytes(n) + fa.sharedSizeBytes;
-    if (need > size_t(optin)) return 0;
-    cudaFuncSetAttribute(k_query_cta<false, T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
-    cudaFuncSetAttribute(k_query_cta<true, T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem_bytes(n)));
+    if (cudaFuncGetAttributes(&fa, k_query_cta<false, T, L, A16, false>) != cudaSuccess) return 0;
+    const size_t smem = cta_smem_bytes(n, A16);
+    if (smem + fa.sharedSizeBytes > size_t(optin)) return 0;
+    cudaFuncSetAttribute(k_query_cta<false, T, L, A16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<false, T, L>, T, cta_smem_bytes(n));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_cta<false, T, L, A16, false>, T, smem);
     return per_sm * sms;
 }
 
-int cta_grid_size(uint32_t n, int variant) {
-    switch (variant) {
-        case 384: return cta_grid_size_t<384, 512>(n);
-        case 256: return cta_grid_size_t<256, 512>(n);
-        default: return cta_grid_size_t<512, 2048>(n);
+template <bool A16>
+int cta_grid_size_a(uint32_t n, int threads) {
+    switch (threads) {
+        case 1024: return cta_grid_size_t<1024, 2048, A16>(n);
+        case 512: return cta_grid_size_t<512, 2048, A16>(n);
+        case 384: return cta_grid_size_t<384, 512, A16>(n);
+        case 192: return cta_grid_size_t<192, 512, A16>(n);
+        case 128: return cta_grid_size_t<128, 512, A16>(n);
+        default: return cta_grid_size_t<256, 512, A16>(n);
     }
+}
+
+int cta_grid_size(uint32_t n, int threads, bool a16) {
+    // the uint16 pass always has the uint32 variant behind it: both must fit
+    const int g32 = cta_grid_size_a<false>(n, threads);
+    if (!a16 || g32 == 0) return g32;
+    return cta_grid_size_a<true>(n, threads);
 }
 
 size_t cta_static_smem() {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_query_cta<false, 512, 2048>);
+    cudaFuncGetAttributes(&fa, k_query_cta<false, 1024, 2048, false, false>);
     return fa.sharedSizeBytes;
 }
 
@@ -571,15 +665,8 @@ cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint
     return cudaGetLastError();
 }
 
-cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_src, const uint32_t *d_ts,
-                             uint64_t nq, uint32_t *d_out, uint32_t *d_sweeps, unsigned long long *d_qcounter,
-                             unsigned long long *d_invalid, int grid_cap, unsigned long long *d_counters,
-                             cudaStream_t st, const uint32_t *d_dst) {
-    (void)subwarp;  // the CTA kernel flattens (vertex, type) pairs: no sub-warps
-    return d_counters ? launch_cta_variant<true>(ix.cta_threads, ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter,
-                                                 d_invalid, grid_cap, d_counters, d_dst, st)
-                      : launch_cta_variant<false>(ix.cta_threads, ix, d_src, d_ts, nq, d_out, d_sweeps, d_qcounter,
-                                                  d_invalid, grid_cap, nullptr, d_dst, st);
+cudaError_t launch_query_cta(const DevIndex &ix, const CtaArgs &a, cudaStream_t st) {
+    return (a.counters && !a.dst) ? launch_cta_variant<true>(ix, a, st) : launch_cta_variant<false>(ix, a, st);
 }
 
 cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,

@@ -13,6 +13,7 @@ struct DevIndex {
     uint32_t cta_threads;       // CTA-kernel variant: 512 (default), 384 or 256 threads per query
     uint32_t cs_magic;          // floor(2^(31+l) / cs) + 1, l = ceil(log2 cs): e / cs == (e * cs_magic) >> (31 + l)
     uint32_t cs_shift;          // 31 + l   (exact for every e < 2^31)
+    uint32_t dense_nc;          // > 0: dense cluster directory, record (t, k) at t*dense_nc + k
     uint64_t num_types;
     const uint32_t *type_ptr;   // [n+1]
     const uint4 *type_rec;      // [2*T]  (32 B per type)
@@ -33,20 +34,32 @@ struct GridWork {
 
 enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2 };
 
-// Largest dynamic shared memory (bytes) the CTA kernel may use on `device`.
-size_t cta_smem_bytes(uint32_t n);
+// Dynamic shared memory of the CTA kernel for n vertices (uint16 or uint32 e[]).
+size_t cta_smem_bytes(uint32_t n, bool a16);
 
 // Cluster-AP lookup for (type, bound) pairs (test entry point).
 cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,
                           uint32_t *d_out, cudaStream_t st);
 
-// One CTA per query, arr in shared memory.  d_qcounter: one uint64 zeroed here.
-// d_counters: NULL, or 6 uint64 work counters accumulated by the instrumented variant.
-// d_dst: NULL (d_out = [nq][n] rows), or per-query targets (d_out = [nq] arrival at the target, pruned search).
-cudaError_t launch_query_cta(const DevIndex &ix, int subwarp, const uint32_t *d_src, const uint32_t *d_ts,
-                             uint64_t nq, uint32_t *d_out, uint32_t *d_sweeps, unsigned long long *d_qcounter,
-                             unsigned long long *d_invalid, int grid_cap, unsigned long long *d_counters,
-                             cudaStream_t st, const uint32_t *d_dst = nullptr);
+// Arguments of the CTA (one query per CTA, e[] in shared memory) kernel.
+struct CtaArgs {
+    const uint32_t *src = nullptr, *ts = nullptr;  // [nq] queries (caller ids / seconds)
+    uint64_t nq = 0;
+    uint32_t *out = nullptr;        // [nq][n] rows, or [nq] arrivals when dst != NULL
+    uint32_t *sweeps = nullptr;     // optional [nq] sweep counts
+    unsigned long long *qcounter = nullptr;  // 1 word, zeroed per launch (dynamic query scheduling)
+    unsigned long long *invalid = nullptr;   // invalid-query counter
+    unsigned long long *counters = nullptr;  // EAT_BUILD_COUNTERS work counters (instrumented variant) or NULL
+    const uint32_t *dst = nullptr;  // goal-directed targets or NULL
+    uint32_t *ovf_list = nullptr;   // [nq] + 1 count word (ovf_cnt): uint16-pass overflow queries
+    uint32_t *ovf_cnt = nullptr;
+    int threads = 256;              // 1024, 512, 384, 256, 192 or 128
+    bool arr16 = false;             // uint16 pass (+ uint32 recompute of overflowing queries)
+    uint64_t grid_cap = 0;
+};
+
+// One CTA per query, e[] in shared memory (kernels.cu).
+cudaError_t launch_query_cta(const DevIndex &ix, const CtaArgs &a, cudaStream_t st);
 
 // Grid-wide persistent kernel for one query with global arr (cooperative launch).
 // subwarp 0: warp-flattened pairs + time window (default); 1..32: virtual warps of that width.
@@ -56,8 +69,8 @@ cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const 
 // CTAs per SM of the persistent grid kernels (env EAT_GRID_CTAS_PER_SM, default 4).
 int grid_ctas_per_sm();
 
-// Occupancy-derived grid size of the CTA kernel variant for n vertices (0 if arr does not fit).
-int cta_grid_size(uint32_t n, int variant);
+// Occupancy-derived grid size of the CTA kernel variant for n vertices (0 if e[] does not fit).
+int cta_grid_size(uint32_t n, int threads, bool a16);
 
 // Static shared memory of the CTA kernel (bytes).
 size_t cta_static_smem();

@@ -47,7 +47,8 @@ class Engine:
                  renumber: str = "auto", kernel: str = "auto", subwarp: int = 0, device: int = -1,
                  host_only: bool = False, counters: bool = False, mode: str = "replicated", part_rank: int = 0, part_count: int = 1,
                  nccl_unique_id: Optional[bytes] = None, window: int = 0,
-                 cta_threads: int = 0, subtrips: int = 0, trip=None):
+                 cta_threads: int = 0, subtrips: int = 0, trip=None, arr_bits: int = 0,
+                 cluster_dir: str = "auto"):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
@@ -70,7 +71,8 @@ class Engine:
                                    mode=_lib.EAT_MODE[mode], part_rank=int(part_rank), part_count=int(part_count),
                                    nccl_unique_id=ctypes.cast(self._nccl_buf, ctypes.c_void_p) if self._nccl_buf else None,
                                    window_seconds=int(window), cta_threads=int(cta_threads),
-                                   subtrips=int(subtrips))
+                                   subtrips=int(subtrips), arr_bits=int(arr_bits),
+                                   cluster_dir={"auto": 0, "dense": 1, "compact": 2}[cluster_dir])
         self._h = _lib.eat_build(tt, opts)
         self.num_vertices = int(num_vertices)
         self.num_connections = int(m)

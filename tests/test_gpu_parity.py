@@ -97,7 +97,8 @@ def test_random_small_instances(kernel):
         tt = synth.random_small(seed)
         eng = Engine.from_timetable(tt, kernel=kernel, cluster_seconds=[3600, 600, 4096, 60][seed % 4],
                                     subwarp=[1, 2, 4, 8, 16, 32, 0, 64][seed % 8],
-                                    cta_threads=[256, 384, 512][seed % 3])
+                                    cta_threads=[256, 384, 512, 192, 128][seed % 5], arr_bits=[16, 32][seed % 2],
+                                    cluster_dir=["auto", "dense", "compact"][seed % 3])
         csa = oracle.CSA(tt.num_vertices, *tt.arrays())
         rng = np.random.default_rng(seed)
         for _ in range(3):
@@ -259,7 +260,8 @@ def test_window_schedules_same_fixpoint(window):
     fixpoint, and so e[], is identical for every window."""
     tt = synth.generate("tiny")
     csa = oracle.CSA(tt.num_vertices, *tt.arrays())
-    eng = Engine.from_timetable(tt, window=window if window else 0x7FFFFFFF, cta_threads=[256, 384, 512][window % 3])
+    eng = Engine.from_timetable(tt, window=window if window else 0x7FFFFFFF, cta_threads=[256, 384, 512][window % 3],
+                                arr_bits=[16, 32][window % 2])
     src, ts = synth.queries(tt, 50, 4)
     _assert_rows(eng.query_many(src, ts), csa.query_many(src, ts), f"window {window}")
     for seed in range(60):
@@ -282,6 +284,30 @@ def test_country_single_query():
         eng = Engine.from_timetable(tt, **kw)
         _assert_rows(eng.query(*synth.SINGLE_QUERY), want, f"country {kw}")
         eng.close()
+
+
+def test_arr16_overflow_recompute():
+    """uint16 e[] offsets: queries whose arrivals pass t_s + 65534 s are
+    recomputed with uint32 e[] (multi-day timetable, t_s = 0); rows exact."""
+    rng = np.random.default_rng(9)
+    n, m = 300, 6000
+    u, v = rng.integers(0, n, m), rng.integers(0, n, m)
+    dep = rng.integers(0, 3 * 86400, m)
+    dur = rng.choice([60, 600, 3600, 7200], m)
+    tt = synth.Timetable(n, *(np.asarray(x, np.uint32) for x in (u, v, dep, dur)))
+    csa = oracle.CSA(n, *tt.arrays())
+    src = rng.integers(0, n, 64).astype(np.uint32)
+    ts = np.where(np.arange(64) % 2 == 0, 0, rng.integers(0, 2 * 86400, 64)).astype(np.uint32)
+    want = csa.query_many(src, ts)
+    assert ((want != INF) & (want - ts[:, None] >= 0xFFFF)).any(), "fixture must overflow uint16 offsets"
+    for bits in (16, 32):
+        eng = Engine.from_timetable(tt, arr_bits=bits)
+        _assert_rows(eng.query_many(src, ts), want, f"arr_bits={bits} multi-day")
+        d = [torch.tensor(x.astype(np.int32), device="cuda") for x in (src, ts)]
+        out = torch.empty((64, n), dtype=torch.int32, device="cuda")
+        eng.query_many_device(d[0], d[1], out)
+        torch.cuda.synchronize()
+        _assert_rows(out.cpu().numpy().astype(np.uint32), want, f"arr_bits={bits} multi-day device")
 
 
 def test_goal_directed_targets():

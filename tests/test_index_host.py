@@ -35,11 +35,11 @@ def _decode(ex, cs):
         v, lam, first, last, cbase, cfirst, u, _ = (int(x) for x in trec[t])
         assert tptr[u] <= t < tptr[u + 1], "type stored under the wrong source vertex"
         deps = []
-        nrec = last // cs - cfirst + 1
-        assert cfirst == first // cs
-        for j in range(nrec):
-            r = crec[cbase + j]
-            k = cfirst + j
+        # compact layout: c_first = first // cs, records crec_base + (k - c_first);
+        # dense directory (the paper's CL[y*i + j]): c_first = 0, crec_base = t * y
+        assert cfirst in (first // cs, 0)
+        for k in range(first // cs, last // cs + 1):
+            r = crec[cbase + k - cfirst]
             if r[1] == 0xFFFFFFFE:
                 items = [int(x) for x in pool[r[2]:r[2] + r[3]]]
             else:
@@ -77,8 +77,8 @@ def _lookup_on_layout(ex, cs, t, b):
     return None if r[0] == INF else int(r[0])
 
 
-def _check_roundtrip(tt, cs=3600, renumber="auto"):
-    eng = Engine.from_timetable(tt, host_only=True, cluster_seconds=cs, renumber=renumber)
+def _check_roundtrip(tt, cs=3600, renumber="auto", cluster_dir="auto"):
+    eng = Engine.from_timetable(tt, host_only=True, cluster_seconds=cs, renumber=renumber, cluster_dir=cluster_dir)
     ex = eng.export()
     perm = ex["perm"].astype(np.int64)
     assert sorted(perm.tolist()) == list(range(tt.num_vertices))
@@ -126,7 +126,8 @@ def test_roundtrip_random_small_cluster_sizes(cs):
         tt = synth.random_small(seed)
         if tt.num_connections == 0:
             continue
-        eng, ex, per_type = _check_roundtrip(tt, cs=cs, renumber=["none", "bfs", "auto"][seed % 3])
+        eng, ex, per_type = _check_roundtrip(tt, cs=cs, renumber=["none", "bfs", "auto"][seed % 3],
+                                             cluster_dir=["auto", "dense", "compact"][seed % 3])
         for t in range(min(len(per_type), 25)):
             deps = per_type[t][3]
             for b in list(range(0, deps[-1] + 2, max(1, cs // 7))) + deps + [d + 1 for d in deps]:
@@ -139,13 +140,13 @@ def test_paper_ap_examples_compress_to_one_item():
     u = [0] * 6
     tt = synth.Timetable(2, np.array(u, np.uint32), np.ones(6, np.uint32), np.arange(10, 36, 5, dtype=np.uint32),
                          np.full(6, 60, np.uint32))
-    ex = Engine.from_timetable(tt, host_only=True, renumber="none").export()
+    ex = Engine.from_timetable(tt, host_only=True, renumber="none", cluster_dir="compact").export()
     items = [int(x) for x in ex["crec"][0][1:] if x != 0xFFFFFFFF]
     assert items == [10 | (5 << 12) | (5 << 24)]  # first 10, difference 5, 6 terms
     deps = np.arange(28800, 64801, 900, dtype=np.uint32)
     tt = synth.Timetable(2, np.zeros(deps.size, np.uint32), np.ones(deps.size, np.uint32), deps,
                          np.full(deps.size, 300, np.uint32))
-    ex = Engine.from_timetable(tt, host_only=True, renumber="none").export()
+    ex = Engine.from_timetable(tt, host_only=True, renumber="none", cluster_dir="compact").export()
     for r in ex["crec"][:-1]:  # hours 8..17: 4 departures each -> one AP item
         assert sum(1 for x in r[1:] if x != 0xFFFFFFFF) == 1
     assert ex["crec"].shape[0] == 11  # clusters 8..18
@@ -156,7 +157,7 @@ def test_next_nonempty_cluster_fallback_layout():
     cluster; records exist from c_first to c_last with next_min precomputed."""
     deps = np.array([100, 3 * 3600 + 5, 3 * 3600 + 65], np.uint32)
     tt = synth.Timetable(2, np.zeros(3, np.uint32), np.ones(3, np.uint32), deps, np.full(3, 60, np.uint32))
-    ex = Engine.from_timetable(tt, host_only=True, renumber="none").export()
+    ex = Engine.from_timetable(tt, host_only=True, renumber="none", cluster_dir="compact").export()
     assert ex["crec"].shape[0] == 4
     assert ex["crec"][0][0] == 3 * 3600 + 5 and ex["crec"][1][0] == 3 * 3600 + 5 and ex["crec"][3][0] == INF
     assert _lookup_on_layout(ex, 3600, 0, 101) == 3 * 3600 + 5
