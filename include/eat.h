@@ -86,9 +86,11 @@ enum {
     EAT_KERNEL_FRONTIER = 1,      /* grid-wide persistent kernel, worklist frontier, global arr */
     EAT_KERNEL_FULL_SWEEP = 2,    /* grid-wide persistent kernel, every type every sweep, active bitmap */
     EAT_KERNEL_CTA = 3,           /* one CTA per query, arr in shared memory */
-    EAT_KERNEL_ASYNC = 4          /* CTA-partitioned: each CTA owns a vertex range (e[] slice in shared
+    EAT_KERNEL_ASYNC = 4,         /* CTA-partitioned: each CTA owns a vertex range (e[] slice in shared
                                      memory), sweeps locally to quiescence, exchanges via global atomicMin
                                      + inboxes; one grid barrier per exchange round */
+    EAT_KERNEL_CONNECTION = 5     /* ablation (NEXT-3): the paper's Connection-version, a thread per raw
+                                     connection every sweep (Algorithm 4) */
 };
 
 /* eat_build_opts.mode */
@@ -127,6 +129,9 @@ typedef struct eat_build_opts {
     uint32_t arr_bits;            /* batched CTA kernel e[] in shared memory: 0/16 -> uint16 offsets from t_s
                                      (twice the queries per SM; a query whose arrivals pass t_s + 65534 s is
                                      recomputed with uint32), 32 -> uint32 only.  Results identical. */
+    uint32_t lookup;              /* grid kernels, ablation (NEXT-3): 0 Cluster-AP;
+                                     1 Connection-type-AP, Algorithm 6 over all AP tuples;
+                                     2 Connection-type, linear getConnection */
     uint32_t cluster_dir;         /* cluster-record addressing: 0 auto (dense for |V| > 52k when it costs <= 3x),
                                      1 dense (record of type t, cluster k at t*y + k -- the paper's CL[y*i+j],
                                      PAPER.md:386-390: fetched in parallel with the type record),

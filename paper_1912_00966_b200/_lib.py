@@ -19,7 +19,7 @@ STATUS_NAMES = ["EAT_OK", "EAT_EINVAL", "EAT_ERANGE", "EAT_ENOMEM", "EAT_ECUDA",
                 "EAT_EUNSUPPORTED", "EAT_ESTATE"]
 
 EAT_RENUMBER = {"auto": 0, "none": 1, "bfs": 2, "morton": 3}
-EAT_KERNEL = {"auto": 0, "frontier": 1, "full_sweep": 2, "cta": 3, "async": 4}
+EAT_KERNEL = {"auto": 0, "frontier": 1, "full_sweep": 2, "cta": 3, "async": 4, "connection": 5}
 EAT_KERNEL_NAMES = {v: k for k, v in EAT_KERNEL.items()}
 EAT_MODE = {"replicated": 0, "edge_partitioned": 1}
 EAT_BUILD_HOST_ONLY = 0x1
@@ -46,7 +46,7 @@ class eat_build_opts(ctypes.Structure):
                 ("mode", ctypes.c_uint32), ("part_rank", ctypes.c_uint32), ("part_count", ctypes.c_uint32),
                 ("nccl_unique_id", ctypes.c_void_p), ("window_seconds", ctypes.c_uint32),
                 ("cta_threads", ctypes.c_uint32), ("subtrips", ctypes.c_uint32),
-                ("arr_bits", ctypes.c_uint32), ("cluster_dir", ctypes.c_uint32)]
+                ("arr_bits", ctypes.c_uint32), ("lookup", ctypes.c_uint32), ("cluster_dir", ctypes.c_uint32)]
 
 
 class eat_stats(ctypes.Structure):

@@ -75,6 +75,9 @@ struct eat_handle {
     uint32_t mode = EAT_MODE_REPLICATED;
     uint32_t window = EAT_INF;           // CTA schedule time window (EAT_INF = all active vertices)
     uint32_t cta_threads = 256;          // CTA-kernel variant (batched queries)
+    uint32_t lookup_mode = 0;            // 0 Cluster-AP; NEXT-3 ablations 1 (Connection-type-AP), 2 (linear)
+    std::vector<uint4> raw;              // EAT_KERNEL_CONNECTION: raw connections until upload
+    uint4 *d_conns = nullptr;
     bool arr16 = true;                   // batched CTA kernel keeps e[] as uint16 offsets (+ uint32 recompute)
     uint32_t *d_ovf[3] = {nullptr, nullptr, nullptr};  // overflow lists: device API, pipeline stages 0/1
     uint64_t ovf_cap[3] = {0, 0, 0};
@@ -117,7 +120,8 @@ void release_device(eat_handle *h) {
     void *ptrs[] = {h->d_perm,  h->gw.arr, h->gw.q0,     h->gw.q1,      h->gw.stamp,   h->gw.bm,
                     h->gw.ctl,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
                     h->d_bsrc[0], h->d_bts[0], h->d_bout[0], h->d_bsrc[1], h->d_bts[1], h->d_bout[1],
-                    h->d_bcounter, h->d_work, h->d_rounds1, h->d_ovf[0], h->d_ovf[1], h->d_ovf[2]};
+                    h->d_bcounter, h->d_work, h->d_rounds1, h->d_ovf[0], h->d_ovf[1], h->d_ovf[2],
+                    h->d_conns};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     eat::async_free(h->aw);
@@ -183,6 +187,7 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     sl.ix.n = n;
     sl.ix.cs = x.cs;
     sl.ix.dense_nc = x.dense_nc;
+    sl.ix.lookup_mode = h->lookup_mode;
     {
         uint32_t l = 0;
         while ((1u << l) < x.cs) ++l;  // ceil(log2 cs)
@@ -295,7 +300,16 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
     if (k == EAT_KERNEL_ASYNC && !async_ok)
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_ASYNC: a 1/SM-count slice of the arrival array does not fit shared memory");
-    if (k > EAT_KERNEL_ASYNC) return fail(EAT_EINVAL, "unknown kernel");
+    if (k > EAT_KERNEL_CONNECTION) return fail(EAT_EINVAL, "unknown kernel");
+    if (k == EAT_KERNEL_CONNECTION) {  // raw connections on the device (ablation schedule)
+        CUDA_TRY(cudaMalloc(&h->d_conns, std::max<size_t>(h->raw.size(), 1) * sizeof(uint4)));
+        CUDA_TRY(cudaMemcpy(h->d_conns, h->raw.data(), h->raw.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+        h->ix.conns = h->d_conns;
+        h->ix.num_conns = h->raw.size();
+        h->slices[0].ix.conns = h->d_conns;
+        h->slices[0].ix.num_conns = h->raw.size();
+        std::vector<uint4>().swap(h->raw);
+    }
     if (k == EAT_KERNEL_ASYNC) {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -340,7 +354,9 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
         CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->aw.ctl + 9, 4, cudaMemcpyDeviceToDevice, st));
         CUDA_TRY(cudaMemcpyAsync(h->d_rounds1, h->aw.ctl + 8, 4, cudaMemcpyDeviceToDevice, st));
     } else {
-        int sched = h->kernel == EAT_KERNEL_FULL_SWEEP ? eat::kSchedFull : eat::kSchedFrontier;
+        int sched = h->kernel == EAT_KERNEL_FULL_SWEEP ? eat::kSchedFull
+                    : h->kernel == EAT_KERNEL_CONNECTION ? eat::kSchedConn
+                                                         : eat::kSchedFrontier;
         CUDA_TRY(eat::launch_query_grid(h->ix, int(h->subwarp), sched, h->gw, s, t_s, d_out, st));
         CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->gw.ctl + 8, 4, cudaMemcpyDeviceToDevice, st));
     }
@@ -368,7 +384,8 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     if (sw != 0 && sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
         return fail(EAT_EINVAL, "subwarp must be 0 (default 32), 1, 2, 4, 8, 16, 32 or 64 (flattened pairs)");
     if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
-    if (o.kernel > EAT_KERNEL_ASYNC) return fail(EAT_EINVAL, "unknown kernel");
+    if (o.kernel > EAT_KERNEL_CONNECTION) return fail(EAT_EINVAL, "unknown kernel");
+    if (o.lookup > 2) return fail(EAT_EINVAL, "lookup must be 0 (Cluster-AP), 1 (Connection-type-AP) or 2 (linear)");
     uint32_t pc = o.part_count ? o.part_count : 1;
     if (o.mode == EAT_MODE_EDGE_PARTITIONED && o.part_rank >= pc)
         return fail(EAT_EINVAL, "edge partition needs part_rank < part_count");
@@ -422,6 +439,14 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     s.num_clusters = h->hx.num_clusters;
     s.num_connections = tt->num_connections;
     s.num_shortcuts = sts.shortcuts;
+    h->lookup_mode = o.lookup;
+    if (o.kernel == EAT_KERNEL_CONNECTION && !h->host_only) {
+        // Connection-version ablation (Alg. 4): keep the raw connections (internal ids)
+        const uint64_t m = tt->num_connections;
+        h->raw.resize(m);
+        for (uint64_t i = 0; i < m; ++i)
+            h->raw[i] = make_uint4(h->hx.perm[tt->u[i]], h->hx.perm[tt->v[i]], tt->dep[i], tt->dep[i] + tt->dur[i]);
+    }
     s.num_types = h->hx.num_types;
     s.num_edges = h->hx.num_edges;
     s.num_cluster_records = h->hx.num_crec;

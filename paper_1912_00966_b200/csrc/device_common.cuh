@@ -112,6 +112,53 @@ __device__ __forceinline__ uint32_t type_next_departure(const DevIndex &ix, cons
     return cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
 }
 
+// Ablation lookups of the paper's incremental versions (NEXT-3), over the
+// same records (so results are identical, only the work differs):
+//   kLookupAP (Connection-type-AP): Algorithm 6 over every
+//     AP tuple of the type, no hour index;
+//   kLookupLinear (Connection-type): getConnection by linear
+//     search over the departures in time order, stopping at the first >= e[u].
+enum { kLookupClusterAP = 0, kLookupAP = 1, kLookupLinear = 2 };
+
+__device__ __forceinline__ uint32_t type_lookup_ablation(const DevIndex &ix, const TypeRec &tr, uint32_t eu,
+                                                         uint32_t mode) {
+    if (eu > tr.last) return kInf;  // early termination in every version
+    uint32_t best = kInf;
+    const uint32_t k0 = cluster_of(ix, tr.first), k1 = cluster_of(ix, tr.last);
+    for (uint32_t k = k0; k <= k1; ++k) {
+        const uint64_t r = uint64_t(tr.crec_base) + (k - tr.c_first);
+        const uint4 r0 = __ldg(ix.crec + 2 * r), r1 = __ldg(ix.crec + 2 * r + 1);
+        const bool spill = r0.y == kItemSpill;
+        const uint32_t nitems = spill ? r0.w : uint32_t(kInlineItems);
+        const uint32_t base = k * ix.cs;
+        for (uint32_t i = 0; i < nitems; ++i) {
+            uint32_t it;
+            if (spill) it = __ldg(ix.pool + r0.z + i);
+            else {
+                const uint32_t v[kInlineItems] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+                it = v[i];
+            }
+            if (it == kItemEmpty) break;
+            const uint32_t off = it & 0xFFFu, stride = (it >> 12) & 0xFFFu, cnt = (it >> 24) + 1u;
+            if (mode == kLookupLinear) {  // enumerate the terms
+                for (uint32_t j = 0; j < cnt; ++j) {
+                    const uint32_t d = base + off + j * stride;
+                    if (d >= eu) {
+                        best = min(best, d);
+                        break;
+                    }
+                }
+            } else {  // Algorithm 6 on this tuple (absolute times)
+                const uint32_t first = base + off, last = first + (cnt - 1u) * stride;
+                if (eu <= first) best = min(best, first);
+                else if (eu <= last) best = min(best, first + ((eu - first + stride - 1u) / stride) * stride);
+            }
+        }
+        if (mode == kLookupLinear && best != kInf) break;  // clusters are in time order
+    }
+    return best;
+}
+
 // ---------------------------------------------------------------- grid barrier
 __device__ __forceinline__ void grid_sync(uint32_t *bar) {
     __syncthreads();
@@ -154,9 +201,11 @@ __device__ __forceinline__ uint32_t relax_type_global(const DevIndex &ix, uint64
     if (eu > tr.last) return kNone;
     const uint32_t av = __ldcg(arr + tr.v);
     if (max(eu, tr.first) + tr.lam >= av) return kNone;  // early termination
-    const uint32_t tc = eu <= tr.first ? tr.first
-                                       : (ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
-                                                      : cluster_lookup(ix, tr.crec_base, tr.c_first, eu));
+    const uint32_t tc = ix.lookup_mode ? type_lookup_ablation(ix, tr, eu, ix.lookup_mode)
+                        : eu <= tr.first ? tr.first
+                                         : (ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
+                                                        : cluster_lookup(ix, tr.crec_base, tr.c_first, eu));
+    if (tc == kInf) return kNone;
     const uint32_t cand = tc + tr.lam;
     if (cand >= av) return kNone;
     const uint32_t old = atomicMin(arr + tr.v, cand);

@@ -395,9 +395,9 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     // Initialize (Algorithm 2)
     for (uint64_t i = gtid; i < n; i += gsz) {
         w.arr[i] = kInf;
-        if (SCHED != kSchedFull) w.stamp[i] = 0;
+        if (SCHED != kSchedFull && SCHED != kSchedConn) w.stamp[i] = 0;
     }
-    if (SCHED == kSchedFull)
+    if (SCHED == kSchedFull || SCHED == kSchedConn)
         for (uint64_t i = gtid; i < 3ull * W; i += gsz) w.bm[i] = 0;
     if (gtid == 0) {
         w.ctl[0] = 1;  // sweep 0 sees one active vertex
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     if (gtid == 0) {
         const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
         w.arr[si] = ts;
-        if (SCHED != kSchedFull) w.q0[0] = si;
+        if (SCHED != kSchedFull && SCHED != kSchedConn) w.q0[0] = si;
         else w.bm[si >> 5] = 1u << (si & 31u);
     }
     grid_sync(bar);
@@ -508,20 +508,26 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
             uint32_t *bo = w.bm + uint64_t(c_old) * W;
             for (uint64_t i = gtid; i < W; i += gsz) bo[i] = 0;
             bool improved = false;
-            for (uint64_t t = gtid; t < ix.num_types; t += gsz) {
-                const uint32_t x = __ldg(ix.type_src + t);
-                if (!((ld_cg(bc + (x >> 5)) >> (x & 31u)) & 1u)) continue;
-                const uint32_t eu = ld_cg(w.arr + x);
-                const TypeRec tr = load_type(ix, t);
-                if (eu > tr.last) continue;
-                const uint32_t av = ld_cg(w.arr + tr.v);
-                if (max(eu, tr.first) + tr.lam >= av) continue;
-                const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
-                const uint32_t cand = tc + tr.lam;
-                if (cand < av) {
-                    const uint32_t old = atomicMin(w.arr + tr.v, cand);
-                    if (cand < old) {
-                        atomicOr(bn + (tr.v >> 5), 1u << (tr.v & 31u));
+            if (SCHED == kSchedConn) {
+                // Connection-version (Algorithm 4): a thread per
+                // connection, Relax (Alg. 3) when its source is active
+                for (uint64_t c = gtid; c < ix.num_conns; c += gsz) {
+                    const uint4 cn = __ldg(ix.conns + c);  // {u, v, dep, arr}
+                    if (!((ld_cg(bc + (cn.x >> 5)) >> (cn.x & 31u)) & 1u)) continue;
+                    if (ld_cg(w.arr + cn.x) > cn.z || cn.w >= ld_cg(w.arr + cn.y)) continue;
+                    if (cn.w < atomicMin(w.arr + cn.y, cn.w)) {
+                        atomicOr(bn + (cn.y >> 5), 1u << (cn.y & 31u));
+                        improved = true;
+                    }
+                }
+            } else {
+                // thread per connection type
+                for (uint64_t t = gtid; t < ix.num_types; t += gsz) {
+                    const uint32_t x = __ldg(ix.type_src + t);
+                    if (!((ld_cg(bc + (x >> 5)) >> (x & 31u)) & 1u)) continue;
+                    const uint32_t v = relax_type_global(ix, t, ld_cg(w.arr + x), w.arr);
+                    if (v != kNone) {
+                        atomicOr(bn + (v >> 5), 1u << (v & 31u));
                         improved = true;
                     }
                 }
@@ -672,6 +678,7 @@ cudaError_t launch_query_cta(const DevIndex &ix, const CtaArgs &a, cudaStream_t 
 cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,
                               uint32_t t_s, uint32_t *d_out, cudaStream_t st) {
     if (sched == kSchedFull) return launch_grid_sw<1, kSchedFull>(ix, w, s, t_s, d_out, st);
+    if (sched == kSchedConn) return launch_grid_sw<1, kSchedConn>(ix, w, s, t_s, d_out, st);
     if (subwarp == 0) return launch_grid_sw<32, kSchedFlat>(ix, w, s, t_s, d_out, st);
     switch (subwarp) {
         case 1: return launch_grid_sw<1, kSchedFrontier>(ix, w, s, t_s, d_out, st);

@@ -14,6 +14,9 @@ struct DevIndex {
     uint32_t cs_magic;          // floor(2^(31+l) / cs) + 1, l = ceil(log2 cs): e / cs == (e * cs_magic) >> (31 + l)
     uint32_t cs_shift;          // 31 + l   (exact for every e < 2^31)
     uint32_t dense_nc;          // > 0: dense cluster directory, record (t, k) at t*dense_nc + k
+    uint32_t lookup_mode;       // 0 Cluster-AP; ablations (grid kernels): 1 Connection-type-AP, 2 Connection-type linear
+    uint64_t num_conns;         // connection-version schedule: raw connections on the device
+    const uint4 *conns;         // [num_conns] {u, v, dep, arr} internal ids (EAT_KERNEL_CONNECTION only)
     uint64_t num_types;
     const uint32_t *type_ptr;   // [n+1]
     const uint4 *type_rec;      // [2*T]  (32 B per type)
@@ -32,7 +35,7 @@ struct GridWork {
     uint32_t *ctl;       // [16] control words: 0-2 rotating counters, 4-5 grid barrier, 8 sweeps, 11-13 window base
 };
 
-enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2 };
+enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2, kSchedConn = 3 };
 
 // Dynamic shared memory of the CTA kernel for n vertices (uint16 or uint32 e[]).
 size_t cta_smem_bytes(uint32_t n, bool a16);
