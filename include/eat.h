@@ -89,8 +89,10 @@ enum {
     EAT_KERNEL_ASYNC = 4,         /* CTA-partitioned: each CTA owns a vertex range (e[] slice in shared
                                      memory), sweeps locally to quiescence, exchanges via global atomicMin
                                      + inboxes; one grid barrier per exchange round */
-    EAT_KERNEL_CONNECTION = 5     /* ablation (NEXT-3): the paper's Connection-version, a thread per raw
+    EAT_KERNEL_CONNECTION = 5,    /* ablation (NEXT-3): the paper's Connection-version, a thread per raw
                                      connection every sweep (Algorithm 4) */
+    EAT_KERNEL_BITMAP = 6         /* grid-wide persistent kernel, global arr, active-vertex bitmap scanned
+                                     by warps (warp per 32-vertex word, lanes over types); no worklist */
 };
 
 /* eat_build_opts.mode */

@@ -300,7 +300,7 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
     if (k == EAT_KERNEL_ASYNC && !async_ok)
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_ASYNC: a 1/SM-count slice of the arrival array does not fit shared memory");
-    if (k > EAT_KERNEL_CONNECTION) return fail(EAT_EINVAL, "unknown kernel");
+    if (k > EAT_KERNEL_BITMAP) return fail(EAT_EINVAL, "unknown kernel");
     if (k == EAT_KERNEL_CONNECTION) {  // raw connections on the device (ablation schedule)
         CUDA_TRY(cudaMalloc(&h->d_conns, std::max<size_t>(h->raw.size(), 1) * sizeof(uint4)));
         CUDA_TRY(cudaMemcpy(h->d_conns, h->raw.data(), h->raw.size() * sizeof(uint4), cudaMemcpyHostToDevice));
@@ -356,6 +356,7 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
     } else {
         int sched = h->kernel == EAT_KERNEL_FULL_SWEEP ? eat::kSchedFull
                     : h->kernel == EAT_KERNEL_CONNECTION ? eat::kSchedConn
+                    : h->kernel == EAT_KERNEL_BITMAP     ? eat::kSchedBitmap
                                                          : eat::kSchedFrontier;
         CUDA_TRY(eat::launch_query_grid(h->ix, int(h->subwarp), sched, h->gw, s, t_s, d_out, st));
         CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->gw.ctl + 8, 4, cudaMemcpyDeviceToDevice, st));
@@ -384,7 +385,7 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     if (sw != 0 && sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
         return fail(EAT_EINVAL, "subwarp must be 0 (default 32), 1, 2, 4, 8, 16, 32 or 64 (flattened pairs)");
     if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
-    if (o.kernel > EAT_KERNEL_CONNECTION) return fail(EAT_EINVAL, "unknown kernel");
+    if (o.kernel > EAT_KERNEL_BITMAP) return fail(EAT_EINVAL, "unknown kernel");
     if (o.lookup > 2) return fail(EAT_EINVAL, "lookup must be 0 (Cluster-AP), 1 (Connection-type-AP) or 2 (linear)");
     uint32_t pc = o.part_count ? o.part_count : 1;
     if (o.mode == EAT_MODE_EDGE_PARTITIONED && o.part_rank >= pc)

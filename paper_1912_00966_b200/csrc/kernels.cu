@@ -395,9 +395,10 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     // Initialize (Algorithm 2)
     for (uint64_t i = gtid; i < n; i += gsz) {
         w.arr[i] = kInf;
-        if (SCHED != kSchedFull && SCHED != kSchedConn) w.stamp[i] = 0;
+        if (SCHED != kSchedFull && SCHED != kSchedConn && SCHED != kSchedBitmap) w.stamp[i] = 0;
     }
-    if (SCHED == kSchedFull || SCHED == kSchedConn)
+    constexpr bool kBitmapSched = SCHED == kSchedFull || SCHED == kSchedConn || SCHED == kSchedBitmap;
+    if (kBitmapSched)
         for (uint64_t i = gtid; i < 3ull * W; i += gsz) w.bm[i] = 0;
     if (gtid == 0) {
         w.ctl[0] = 1;  // sweep 0 sees one active vertex
@@ -411,7 +412,7 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     if (gtid == 0) {
         const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
         w.arr[si] = ts;
-        if (SCHED != kSchedFull && SCHED != kSchedConn) w.q0[0] = si;
+        if (!kBitmapSched) w.q0[0] = si;
         else w.bm[si >> 5] = 1u << (si & 31u);
     }
     grid_sync(bar);
@@ -508,7 +509,29 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
             uint32_t *bo = w.bm + uint64_t(c_old) * W;
             for (uint64_t i = gtid; i < W; i += gsz) bo[i] = 0;
             bool improved = false;
-            if (SCHED == kSchedConn) {
+            if (SCHED == kSchedBitmap) {
+                // bitmap frontier: a warp per 32-vertex word of the active bitmap,
+                // lanes over the types of each active vertex; an improvement only
+                // sets the target's bit (no worklist, no stamps)
+                const uint32_t lane = threadIdx.x & 31u;
+                for (uint64_t wd = gtid >> 5; wd < W; wd += gsz >> 5) {
+                    uint32_t word = ld_cg(bc + wd);
+                    while (word) {
+                        const uint32_t b = __ffs(word) - 1u;
+                        word &= word - 1u;
+                        const uint32_t x = uint32_t(wd) * 32u + b;
+                        const uint32_t eu = ld_cg(w.arr + x);
+                        const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
+                        for (uint32_t t = p0 + lane; t < p1; t += 32u) {
+                            const uint32_t v = relax_type_global(ix, t, eu, w.arr);
+                            if (v != kNone) {
+                                atomicOr(bn + (v >> 5), 1u << (v & 31u));
+                                improved = true;
+                            }
+                        }
+                    }
+                }
+            } else if (SCHED == kSchedConn) {
                 // Connection-version (Algorithm 4): a thread per
                 // connection, Relax (Alg. 3) when its source is active
                 for (uint64_t c = gtid; c < ix.num_conns; c += gsz) {
@@ -679,6 +702,7 @@ cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const 
                               uint32_t t_s, uint32_t *d_out, cudaStream_t st) {
     if (sched == kSchedFull) return launch_grid_sw<1, kSchedFull>(ix, w, s, t_s, d_out, st);
     if (sched == kSchedConn) return launch_grid_sw<1, kSchedConn>(ix, w, s, t_s, d_out, st);
+    if (sched == kSchedBitmap) return launch_grid_sw<32, kSchedBitmap>(ix, w, s, t_s, d_out, st);
     if (subwarp == 0) return launch_grid_sw<32, kSchedFlat>(ix, w, s, t_s, d_out, st);
     switch (subwarp) {
         case 1: return launch_grid_sw<1, kSchedFrontier>(ix, w, s, t_s, d_out, st);

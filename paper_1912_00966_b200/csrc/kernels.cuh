@@ -35,7 +35,7 @@ struct GridWork {
     uint32_t *ctl;       // [16] control words: 0-2 rotating counters, 4-5 grid barrier, 8 sweeps, 11-13 window base
 };
 
-enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2, kSchedConn = 3 };
+enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2, kSchedConn = 3, kSchedBitmap = 4 };
 
 // Dynamic shared memory of the CTA kernel for n vertices (uint16 or uint32 e[]).
 size_t cta_smem_bytes(uint32_t n, bool a16);

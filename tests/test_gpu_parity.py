@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_1912_00966_b200 import Engine, EatError, _lib  # noqa: E402
 
-KERNELS = ["cta", "frontier", "full_sweep", "async"]
+KERNELS = ["cta", "frontier", "full_sweep", "async", "bitmap"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -284,6 +284,25 @@ def test_country_single_query():
         eng = Engine.from_timetable(tt, **kw)
         _assert_rows(eng.query(*synth.SINGLE_QUERY), want, f"country {kw}")
         eng.close()
+
+
+@pytest.mark.parametrize("kw", [dict(kernel="connection"), dict(kernel="full_sweep", lookup="linear"),
+                                dict(kernel="full_sweep", lookup="ap"), dict(kernel="frontier", lookup="linear"),
+                                dict(kernel="frontier", lookup="ap", subwarp=4)])
+def test_ablation_versions(kw):
+    """NEXT-3: the paper's incremental versions (Alg. 4, Alg. 5 linear, Alg. 6
+    over all APs) give the oracle's arrival times too."""
+    tt = synth.generate("tiny")
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    eng = Engine.from_timetable(tt, **kw)
+    for s, t_s in [synth.SINGLE_QUERY, (50, 40000), (199, 80000)]:
+        _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"ablation {kw} ({s},{t_s})")
+    for seed in range(60):
+        t2 = synth.random_small(7000 + seed)
+        c2 = oracle.CSA(t2.num_vertices, *t2.arrays())
+        e2 = Engine.from_timetable(t2, cluster_seconds=[3600, 600][seed % 2], **kw)
+        s, t_s = seed % t2.num_vertices, (seed * 4099) % 86400
+        _assert_rows(e2.query(s, t_s), c2.query(s, t_s), f"ablation {kw} seed {seed}")
 
 
 def test_arr16_overflow_recompute():
