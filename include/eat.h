@@ -138,6 +138,9 @@ typedef struct eat_build_opts {
                                      1 dense (record of type t, cluster k at t*y + k -- the paper's CL[y*i+j],
                                      PAPER.md:386-390: fetched in parallel with the type record),
                                      2 compact (records only for [c_first, c_last] of each type) */
+    uint32_t continuation;        /* CTA kernel: 0/1 on, 2 off.  A vertex a warp lowers inside the current
+                                     window is relaxed again by that warp in the same sweep (claimed from
+                                     the frontier), so chains advance several hops per sweep. */
 } eat_build_opts;
 
 #define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */

@@ -46,7 +46,8 @@ class eat_build_opts(ctypes.Structure):
                 ("mode", ctypes.c_uint32), ("part_rank", ctypes.c_uint32), ("part_count", ctypes.c_uint32),
                 ("nccl_unique_id", ctypes.c_void_p), ("window_seconds", ctypes.c_uint32),
                 ("cta_threads", ctypes.c_uint32), ("subtrips", ctypes.c_uint32),
-                ("arr_bits", ctypes.c_uint32), ("lookup", ctypes.c_uint32), ("cluster_dir", ctypes.c_uint32)]
+                ("arr_bits", ctypes.c_uint32), ("lookup", ctypes.c_uint32), ("cluster_dir", ctypes.c_uint32),
+                ("continuation", ctypes.c_uint32)]
 
 
 class eat_stats(ctypes.Structure):

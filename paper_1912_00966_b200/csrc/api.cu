@@ -76,6 +76,7 @@ struct eat_handle {
     uint32_t window = EAT_INF;           // CTA schedule time window (EAT_INF = all active vertices)
     uint32_t cta_threads = 256;          // CTA-kernel variant (batched queries)
     uint32_t lookup_mode = 0;            // 0 Cluster-AP; NEXT-3 ablations 1 (Connection-type-AP), 2 (linear)
+    uint32_t cont = 1;                   // CTA kernel: warp-local continuation
     std::vector<uint4> raw;              // EAT_KERNEL_CONNECTION: raw connections until upload
     uint4 *d_conns = nullptr;
     bool arr16 = true;                   // batched CTA kernel keeps e[] as uint16 offsets (+ uint32 recompute)
@@ -188,6 +189,7 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     sl.ix.cs = x.cs;
     sl.ix.dense_nc = x.dense_nc;
     sl.ix.lookup_mode = h->lookup_mode;
+    sl.ix.cont = h->cont;
     {
         uint32_t l = 0;
         while ((1u << l) < x.cs) ++l;  // ceil(log2 cs)
@@ -405,7 +407,12 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
         delete h;
         return fail(EAT_EINVAL, "arr_bits must be 0, 16 or 32");
     }
-    h->arr16 = o.arr_bits == 16;  // default uint32 (tools/sweep_cta.py: uint16 gives no gain)
+    h->arr16 = o.arr_bits == 16;
+    if (o.continuation > 2) {
+        delete h;
+        return fail(EAT_EINVAL, "continuation must be 0 (default), 1 (on) or 2 (off)");
+    }
+    h->cont = o.continuation == 2 ? 0u : 1u;  // default uint32 (tools/sweep_cta.py: uint16 gives no gain)
     h->part_rank = o.part_rank;
     h->part_count = pc;
     h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 && !o.nccl_unique_id;

@@ -132,6 +132,8 @@ struct SArr<true> {
 template <int T, bool A16>
 constexpr int cta_min_blocks() { return T >= 1024 ? 1 : (A16 ? 8 : (T >= 512 ? 4 : 5)); }
 
+constexpr uint32_t kLocalQ = 16;
+
 template <bool COUNT, int kCtaThreads, int kListCap, bool A16, bool TGT>
 __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>())) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
                                                                const uint32_t *__restrict__ tsv, uint64_t nq,
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
     uint32_t *bmD = sm + SArr<A16>::bytes(n) / 4u;  // deferred: active, not yet selected
     uint32_t *bmN = bmD + W;    // new: lowered since their last selection
     __shared__ uint32_t s_list[kListCap];
+    __shared__ uint32_t s_lq[kCtaWarps * kLocalQ];  // warp-local continuation queues
     __shared__ uint32_t s_cnt[2], s_more[2];  // per sweep parity: listed / (deferred + improved)
     __shared__ uint32_t s_tmin[3];            // window base, rotating per sweep
     __shared__ uint32_t s_ovf;                // A16: an arrival offset overflowed
@@ -277,14 +280,41 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             const uint32_t F = min(s_cnt[p], uint32_t(kListCap));
             // ---- 2. warp-level flattened (vertex, type) pairs; a warp takes g
             // consecutive list entries so that small frontiers still spread
-            // over all warps
+            // over all warps.  Continuation (ix.cont): a vertex the warp lowers
+            // within the current window goes to a small warp-local queue and is
+            // relaxed by the same warp in this sweep (claimed by clearing its
+            // new-bit), so a chain of improvements advances several hops per
+            // sweep instead of one.
             const uint32_t g = min(32u, max(1u, (F + kCtaWarps - 1u) / kCtaWarps));
             uint32_t nimpr = 0;
-            for (uint32_t k0 = wid * g; k0 < F; k0 += kCtaWarps * g) {
-                const uint32_t j = k0 + lane;
+            uint32_t k0 = wid * g;
+            uint32_t lq_cnt = 0;  // warp-uniform
+            uint32_t *lq = s_lq + wid * kLocalQ;
+            for (;;) {
                 uint32_t x = 0, p0 = 0, nt = 0;
-                if (lane < g && j < F) {
-                    x = s_list[j];
+                bool valid = false;
+                if (k0 < F) {
+                    const uint32_t j = k0 + lane;
+                    valid = lane < g && j < F;
+                    if (valid) x = s_list[j];
+                    k0 += kCtaWarps * g;
+                } else if (lq_cnt > 0) {
+                    const uint32_t take = min(lq_cnt, 32u);
+                    if (lane < take) {
+                        x = lq[lq_cnt - take + lane];
+                        const uint32_t bit = 1u << (x & 31u);
+                        valid = (atomicAnd(bmN + (x >> 5), ~bit) & bit) != 0u;  // claim
+                        if (valid && thr < kInf && ar.get(x) > thr) {  // left the window: next sweeps
+                            atomicOr(bmN + (x >> 5), bit);
+                            valid = false;
+                        }
+                    }
+                    lq_cnt -= take;
+                    __syncwarp();
+                } else {
+                    break;
+                }
+                if (valid) {
                     p0 = __ldg(ix.type_ptr + x);
                     nt = __ldg(ix.type_ptr + x + 1) - p0;
                     if (COUNT) ++c_vis;
@@ -309,38 +339,51 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
                     const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
                     const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
-                    if (qp >= tot) continue;
-                    const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
-                    const uint32_t eu = ar.get(u);
-                    CrecPrefetch pf{};
-                    if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the type record
-                    const TypeRec tr = load_type(ix, t);
-                    if (COUNT) ++c_type;
-                    if (eu > tr.last) continue;
-                    const uint32_t av = ar.get(tr.v);
-                    const uint32_t lim = TGT ? min(av, ar.get(di)) : av;
-                    if (max(eu, tr.first) + tr.lam >= lim) continue;  // PAPER.md:411-416 (+ target bound)
-                    uint32_t tc;
-                    if (eu <= tr.first) {
-                        tc = tr.first;
-                    } else {
-                        tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
-                                         : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
-                        if (COUNT) {
-                            ++c_crec;
-                            const uint4 rr = __ldg(ix.crec + 2ull * (tr.crec_base + cluster_of(ix, eu) - tr.c_first));
-                            if (rr.y == kItemSpill) c_spill += rr.w;
+                    uint32_t pushv = kNone;
+                    do {
+                        if (qp >= tot) break;
+                        const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
+                        const uint32_t eu = ar.get(u);
+                        CrecPrefetch pf{};
+                        if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the type record
+                        const TypeRec tr = load_type(ix, t);
+                        if (COUNT) ++c_type;
+                        if (eu > tr.last) break;
+                        const uint32_t av = ar.get(tr.v);
+                        const uint32_t lim = TGT ? min(av, ar.get(di)) : av;
+                        if (max(eu, tr.first) + tr.lam >= lim) break;  // PAPER.md:411-416 (+ target bound)
+                        uint32_t tc;
+                        if (eu <= tr.first) {
+                            tc = tr.first;
+                        } else {
+                            tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
+                                             : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                            if (COUNT) {
+                                ++c_crec;
+                                const uint4 rr = __ldg(ix.crec + 2ull * (tr.crec_base + cluster_of(ix, eu) - tr.c_first));
+                                if (rr.y == kItemSpill) c_spill += rr.w;
+                            }
                         }
-                    }
-                    const uint32_t cand = tc + tr.lam;
-                    if (cand < av) {
-                        const uint32_t old = ar.amin(tr.v, cand, &s_ovf);
-                        if (cand < old) {
-                            atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
-                            if (window < kInf) atomicMin(&s_tmin[t_nxt], cand);
-                            ++nimpr;
-                            if (COUNT) ++c_impr;
+                        const uint32_t cand = tc + tr.lam;
+                        if (cand < av) {
+                            const uint32_t old = ar.amin(tr.v, cand, &s_ovf);
+                            if (cand < old) {
+                                atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
+                                if (window < kInf) atomicMin(&s_tmin[t_nxt], cand);
+                                ++nimpr;
+                                if (COUNT) ++c_impr;
+                                if (cand <= thr) pushv = tr.v;
+                            }
                         }
+                    } while (0);
+                    if (ix.cont) {  // append this round's improvements to the warp-local queue
+                        const unsigned m = __ballot_sync(0xFFFFFFFFu, pushv != kNone);
+                        if (m) {
+                            const uint32_t pos = lq_cnt + __popc(m & ((1u << lane) - 1u));
+                            if (pushv != kNone && pos < kLocalQ) lq[pos] = pushv;
+                            lq_cnt = min(uint32_t(kLocalQ), lq_cnt + uint32_t(__popc(m)));
+                        }
+                        __syncwarp();
                     }
                 }
             }
