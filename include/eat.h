@@ -138,7 +138,7 @@ typedef struct eat_build_opts {
                                      1 dense (record of type t, cluster k at t*y + k -- the paper's CL[y*i+j],
                                      PAPER.md:386-390: fetched in parallel with the type record),
                                      2 compact (records only for [c_first, c_last] of each type) */
-    uint32_t continuation;        /* CTA kernel: 0/1 on, 2 off.  A vertex a warp lowers inside the current
+    uint32_t continuation;        /* CTA kernel: 0/2 off, 1 on.  A vertex a warp lowers inside the current
                                      window is relaxed again by that warp in the same sweep (claimed from
                                      the frontier), so chains advance several hops per sweep. */
 } eat_build_opts;
@@ -235,6 +235,10 @@ typedef struct eat_stats {
     uint64_t improvements;        /* successful atomicMin relaxations */
     uint64_t sweeps_total;        /* relaxation sweeps summed over queries */
     uint64_t num_shortcuts;       /* sub-trip shortcut connections added at build (indexed with the rest) */
+    uint64_t select_cycles;       /* EAT_BUILD_COUNTERS: SM clock cycles of the CTA kernel's select phases */
+    uint64_t pair_cycles;         /*   ... and of its relaxation (pair) phases, summed over queries */
+    uint64_t select_loop_cycles;  /*   ... slowest warp's own work inside the select phases (rest = barrier) */
+    uint64_t pair_loop_cycles;    /*   ... slowest warp's own work inside the pair phases */
 } eat_stats;
 
 eat_status eat_get_stats(const eat_handle *h, eat_stats *out);

@@ -61,7 +61,9 @@ class eat_stats(ctypes.Structure):
                 ("smem_vertices_max", ctypes.c_uint32), ("vertex_visits", ctypes.c_uint64),
                 ("type_evals", ctypes.c_uint64), ("cluster_reads", ctypes.c_uint64),
                 ("spill_items_read", ctypes.c_uint64), ("improvements", ctypes.c_uint64),
-                ("sweeps_total", ctypes.c_uint64), ("num_shortcuts", ctypes.c_uint64)]
+                ("sweeps_total", ctypes.c_uint64), ("num_shortcuts", ctypes.c_uint64),
+                ("select_cycles", ctypes.c_uint64), ("pair_cycles", ctypes.c_uint64),
+                ("select_loop_cycles", ctypes.c_uint64), ("pair_loop_cycles", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

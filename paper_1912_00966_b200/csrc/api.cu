@@ -412,7 +412,7 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
         delete h;
         return fail(EAT_EINVAL, "continuation must be 0 (default), 1 (on) or 2 (off)");
     }
-    h->cont = o.continuation == 2 ? 0u : 1u;  // default uint32 (tools/sweep_cta.py: uint16 gives no gain)
+    h->cont = o.continuation == 1 ? 1u : 0u;  // default off (tools/sweep_cont.py: fewer sweeps, slower)  // default uint32 (tools/sweep_cta.py: uint16 gives no gain)
     h->part_rank = o.part_rank;
     h->part_count = pc;
     h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 && !o.nccl_unique_id;
@@ -490,8 +490,8 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
         est = resolve_kernel(h, o.kernel);
         if (est != EAT_OK) break;
         if (o.flags & EAT_BUILD_COUNTERS) {
-            if (cudaMalloc(&h->d_work, 6 * sizeof(unsigned long long)) != cudaSuccess ||
-                cudaMemset(h->d_work, 0, 6 * sizeof(unsigned long long)) != cudaSuccess) {
+            if (cudaMalloc(&h->d_work, 10 * sizeof(unsigned long long)) != cudaSuccess ||
+                cudaMemset(h->d_work, 0, 10 * sizeof(unsigned long long)) != cudaSuccess) {
                 est = fail(EAT_ENOMEM, "cannot allocate work counters");
                 break;
             }
@@ -543,8 +543,12 @@ eat_status eat_get_stats(const eat_handle *hc, eat_stats *out) {
             h->st.last_rounds = rr;
         }
         if (h->d_work) {
-            unsigned long long w[6];
+            unsigned long long w[10];
             CUDA_TRY(cudaMemcpy(w, h->d_work, sizeof(w), cudaMemcpyDeviceToHost));
+            h->st.select_cycles = w[6];
+            h->st.pair_cycles = w[7];
+            h->st.select_loop_cycles = w[8];
+            h->st.pair_loop_cycles = w[9];
             h->st.vertex_visits = w[0];
             h->st.type_evals = w[1];
             h->st.cluster_reads = w[2];

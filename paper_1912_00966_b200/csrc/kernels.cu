@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
     __shared__ uint32_t s_cnt[2], s_more[2];  // per sweep parity: listed / (deferred + improved)
     __shared__ uint32_t s_tmin[3];            // window base, rotating per sweep
     __shared__ uint32_t s_ovf;                // A16: an arrival offset overflowed
+    __shared__ unsigned long long s_tw[2];    // COUNT: slowest warp's select / pair loop cycles
     __shared__ unsigned long long s_q;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
     const uint32_t window = ix.window;
@@ -215,6 +216,9 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
         const uint32_t di = TGT ? __ldg(ix.perm + dq) : 0u;
         uint32_t sweeps = 0;
         uint32_t c_vis = 0, c_type = 0, c_crec = 0, c_spill = 0, c_impr = 0;
+        unsigned long long c_sel_cyc = 0, c_pair_cyc = 0, t_mark = COUNT ? clock64() : 0;
+        unsigned long long c_sel_loop = 0, c_pair_loop = 0;  // slowest warp's own loop time
+        if (COUNT && tid == 0) s_tw[0] = s_tw[1] = 0;
         for (;;) {
             const uint32_t p = sweeps & 1u;
             const uint32_t t_nxt = (sweeps + 1u) % 3u;  // s_tmin slot written by this sweep
@@ -225,46 +229,64 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             }
             // goal-directed: a vertex with e[u] >= e[dst] cannot lower e[dst]
             const uint32_t best = TGT ? ar.get(di) : uint32_t(kInf);
-            // ---- 1. select + compact: active = deferred | new
+            const unsigned long long t_sw0 = COUNT ? clock64() : 0ull;
+            // ---- 1. select + compact: active = deferred | new.  The word loop is
+            // warp-uniform so that list slots are allocated with one shared
+            // atomic per warp (warp prefix sum of the selected-bit counts).
             uint32_t dmin = kInf, ndef = 0;
-            for (uint32_t w = tid; w < W; w += kCtaThreads) {
-                uint32_t word = bmD[w] | bmN[w];
-                if (!word) continue;
-                bmN[w] = 0;
+            for (uint32_t w0 = 0; w0 < W; w0 += kCtaThreads) {
+                const uint32_t w = w0 + tid;
+                uint32_t word = w < W ? (bmD[w] | bmN[w]) : 0u;
                 uint32_t sel = word;
-                if (thr < kInf || (TGT && best < kInf)) {
-                    sel = 0;
-                    uint32_t rest = word;
-                    while (rest) {
-                        const uint32_t b = __ffs(rest) - 1u;
-                        rest &= rest - 1u;
-                        const uint32_t a = ar.get(w * 32u + b);
-                        if (TGT && a >= best) word &= ~(1u << b);  // pruned for good
-                        else if (a <= thr) sel |= 1u << b;
-                        else dmin = min(dmin, a);
+                if (word) {
+                    bmN[w] = 0;
+                    if (thr < kInf || (TGT && best < kInf)) {
+                        sel = 0;
+                        uint32_t rest = word;
+                        while (rest) {
+                            const uint32_t b = __ffs(rest) - 1u;
+                            rest &= rest - 1u;
+                            const uint32_t a = ar.get(w * 32u + b);
+                            if (TGT && a >= best) word &= ~(1u << b);  // pruned for good
+                            else if (a <= thr) sel |= 1u << b;
+                            else dmin = min(dmin, a);
+                        }
                     }
                 }
-                uint32_t taken = 0;
                 const uint32_t k = __popc(sel);
-                if (k) {
-                    const uint32_t pos = atomicAdd(&s_cnt[p], k);
-                    const uint32_t put = pos < uint32_t(kListCap) ? min(k, uint32_t(kListCap) - pos) : 0u;
-                    uint32_t rest = sel;
-                    for (uint32_t i = 0; i < put; ++i) {
-                        const uint32_t b = __ffs(rest) - 1u;
-                        rest &= rest - 1u;
-                        s_list[pos + i] = w * 32u + b;
-                        taken |= 1u << b;
-                    }
-                    while (rest) {  // list full: stays active for a later sweep
-                        const uint32_t b = __ffs(rest) - 1u;
-                        rest &= rest - 1u;
-                        dmin = min(dmin, ar.get(w * 32u + b));
-                    }
+                uint32_t incl = k;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= uint32_t(o)) incl += y;
                 }
-                bmD[w] = word & ~taken;
-                ndef += __popc(word & ~taken);
+                const uint32_t wtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                uint32_t wbase = 0;
+                if (lane == 0 && wtot) wbase = atomicAdd(&s_cnt[p], wtot);
+                wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
+                if (word) {
+                    uint32_t taken = 0;
+                    if (k) {
+                        const uint32_t pos = wbase + incl - k;
+                        const uint32_t put = pos < uint32_t(kListCap) ? min(k, uint32_t(kListCap) - pos) : 0u;
+                        uint32_t rest = sel;
+                        for (uint32_t i = 0; i < put; ++i) {
+                            const uint32_t b = __ffs(rest) - 1u;
+                            rest &= rest - 1u;
+                            s_list[pos + i] = w * 32u + b;
+                            taken |= 1u << b;
+                        }
+                        while (rest) {  // list full: stays active for a later sweep
+                            const uint32_t b = __ffs(rest) - 1u;
+                            rest &= rest - 1u;
+                            dmin = min(dmin, ar.get(w * 32u + b));
+                        }
+                    }
+                    bmD[w] = word & ~taken;
+                    ndef += __popc(word & ~taken);
+                }
             }
+            if (COUNT && lane == 0) atomicMax(&s_tw[0], clock64() - t_sw0);
             if (window < kInf) {
                 dmin = __reduce_min_sync(0xFFFFFFFFu, dmin);
                 if (lane == 0 && dmin < kInf) atomicMin(&s_tmin[t_nxt], dmin);
@@ -272,6 +294,14 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             ndef = __reduce_add_sync(0xFFFFFFFFu, ndef);
             if (lane == 0 && ndef) atomicAdd(&s_more[p], ndef);
             __syncthreads();
+            if (COUNT && tid == 0) {
+                const unsigned long long now = clock64();
+                c_sel_cyc += now - t_mark;
+                t_mark = now;
+                c_sel_loop += s_tw[0];
+                s_tw[0] = 0;
+            }
+            const unsigned long long t_pr0 = COUNT ? clock64() : 0ull;
             if (tid == 0) {  // slots of the next sweep: everyone is past their last read
                 s_cnt[p ^ 1u] = 0;
                 s_more[p ^ 1u] = 0;
@@ -286,7 +316,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             // new-bit), so a chain of improvements advances several hops per
             // sweep instead of one.
             const uint32_t g = min(32u, max(1u, (F + kCtaWarps - 1u) / kCtaWarps));
-            uint32_t nimpr = 0;
+            uint32_t nimpr = 0, cmin = kInf;
             uint32_t k0 = wid * g;
             uint32_t lq_cnt = 0;  // warp-uniform
             uint32_t *lq = s_lq + wid * kLocalQ;
@@ -369,7 +399,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                             const uint32_t old = ar.amin(tr.v, cand, &s_ovf);
                             if (cand < old) {
                                 atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
-                                if (window < kInf) atomicMin(&s_tmin[t_nxt], cand);
+                                cmin = min(cmin, cand);
                                 ++nimpr;
                                 if (COUNT) ++c_impr;
                                 if (cand <= thr) pushv = tr.v;
@@ -387,9 +417,21 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     }
                 }
             }
+            if (COUNT && lane == 0) atomicMax(&s_tw[1], clock64() - t_pr0);
             nimpr = __reduce_add_sync(0xFFFFFFFFu, nimpr);
             if (lane == 0 && nimpr) atomicAdd(&s_more[p], nimpr);
+            if (window < kInf) {  // window base of the next sweep: one shared atomic per warp
+                cmin = __reduce_min_sync(0xFFFFFFFFu, cmin);
+                if (lane == 0 && cmin < kInf) atomicMin(&s_tmin[t_nxt], cmin);
+            }
             __syncthreads();
+            if (COUNT && tid == 0) {
+                const unsigned long long now = clock64();
+                c_pair_cyc += now - t_mark;
+                t_mark = now;
+                c_pair_loop += s_tw[1];
+                s_tw[1] = 0;
+            }
             ++sweeps;
             if (s_more[p] == 0u) break;  // nothing deferred, nothing lowered: fixpoint
             if (A16 && s_ovf) break;      // recomputed by the uint32 variant
@@ -412,7 +454,13 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                 for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o);
                 if (lane == 0 && v[k]) atomicAdd(counters + k, v[k]);
             }
-            if (tid == 0) atomicAdd(counters + 5, (unsigned long long)sweeps);
+            if (tid == 0) {
+                atomicAdd(counters + 5, (unsigned long long)sweeps);
+                atomicAdd(counters + 6, c_sel_cyc);
+                atomicAdd(counters + 7, c_pair_cyc);
+                atomicAdd(counters + 8, c_sel_loop);
+                atomicAdd(counters + 9, c_pair_loop);
+            }
         }
         __syncthreads();
     }

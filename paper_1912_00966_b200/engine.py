@@ -48,7 +48,7 @@ class Engine:
                  host_only: bool = False, counters: bool = False, mode: str = "replicated", part_rank: int = 0, part_count: int = 1,
                  nccl_unique_id: Optional[bytes] = None, window: int = 0,
                  cta_threads: int = 0, subtrips: int = 0, trip=None, arr_bits: int = 0,
-                 cluster_dir: str = "auto", lookup: str = "cluster_ap", continuation: bool = True):
+                 cluster_dir: str = "auto", lookup: str = "cluster_ap", continuation: bool = False):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
