@@ -43,7 +43,7 @@ extern "C" {
 #endif
 
 #define EAT_INF 0x7FFFFFFFu
-#define EAT_ABI_VERSION 1u
+#define EAT_ABI_VERSION 2u
 
 typedef enum eat_status {
     EAT_OK = 0,
@@ -138,9 +138,8 @@ typedef struct eat_build_opts {
                                      1 dense (record of type t, cluster k at t*y + k -- the paper's CL[y*i+j],
                                      PAPER.md:386-390: fetched in parallel with the type record),
                                      2 compact (records only for [c_first, c_last] of each type) */
-    uint32_t continuation;        /* CTA kernel: 0/2 off, 1 on.  A vertex a warp lowers inside the current
-                                     window is relaxed again by that warp in the same sweep (claimed from
-                                     the frontier), so chains advance several hops per sweep. */
+    uint32_t continuation;        /* 0 or 2.  1 (warp-local continuation of improvements inside a sweep) was
+                                     an experiment of round 1, measured slower and removed: EAT_EUNSUPPORTED. */
 } eat_build_opts;
 
 #define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */
@@ -239,6 +238,8 @@ typedef struct eat_stats {
     uint64_t pair_cycles;         /*   ... and of its relaxation (pair) phases, summed over queries */
     uint64_t select_loop_cycles;  /*   ... slowest warp's own work inside the select phases (rest = barrier) */
     uint64_t pair_loop_cycles;    /*   ... slowest warp's own work inside the pair phases */
+    uint32_t cta_grid;            /* resident CTAs (= queries in flight) of the batched CTA kernel; 0 if e[] does not fit */
+    uint32_t reserved0;
 } eat_stats;
 
 eat_status eat_get_stats(const eat_handle *h, eat_stats *out);

@@ -63,7 +63,8 @@ class eat_stats(ctypes.Structure):
                 ("spill_items_read", ctypes.c_uint64), ("improvements", ctypes.c_uint64),
                 ("sweeps_total", ctypes.c_uint64), ("num_shortcuts", ctypes.c_uint64),
                 ("select_cycles", ctypes.c_uint64), ("pair_cycles", ctypes.c_uint64),
-                ("select_loop_cycles", ctypes.c_uint64), ("pair_loop_cycles", ctypes.c_uint64)]
+                ("select_loop_cycles", ctypes.c_uint64), ("pair_loop_cycles", ctypes.c_uint64),
+                ("cta_grid", ctypes.c_uint32), ("reserved0", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -76,7 +77,6 @@ struct eat_handle {
     uint32_t window = EAT_INF;           // CTA schedule time window (EAT_INF = all active vertices)
     uint32_t cta_threads = 256;          // CTA-kernel variant (batched queries)
     uint32_t lookup_mode = 0;            // 0 Cluster-AP; NEXT-3 ablations 1 (Connection-type-AP), 2 (linear)
-    uint32_t cont = 1;                   // CTA kernel: warp-local continuation
     std::vector<uint4> raw;              // EAT_KERNEL_CONNECTION: raw connections until upload
     uint4 *d_conns = nullptr;
     bool arr16 = true;                   // batched CTA kernel keeps e[] as uint16 offsets (+ uint32 recompute)
@@ -105,6 +105,11 @@ struct eat_handle {
     uint32_t *h_stage[2] = {nullptr, nullptr};
     unsigned long long *d_bcounter = nullptr;  // [2]
     uint64_t bcap = 0, stage_cap = 0;
+    // direct mode (pinned host output, CTA kernel): all queries in one launch,
+    // rows stored by the kernel straight into the mapped host buffer
+    uint32_t *d_dsrc = nullptr, *d_dts = nullptr;
+    uint64_t dcap = 0;
+    bool e2e_direct = true;
     int cta_grid = 0;
     // edge partition
     uint32_t part_rank = 0, part_count = 1, part_lo = 0, part_hi = 0;
@@ -122,7 +127,7 @@ void release_device(eat_handle *h) {
                     h->gw.ctl,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
                     h->d_bsrc[0], h->d_bts[0], h->d_bout[0], h->d_bsrc[1], h->d_bts[1], h->d_bout[1],
                     h->d_bcounter, h->d_work, h->d_rounds1, h->d_ovf[0], h->d_ovf[1], h->d_ovf[2],
-                    h->d_conns};
+                    h->d_conns, h->d_dsrc, h->d_dts};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     eat::async_free(h->aw);
@@ -189,7 +194,6 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     sl.ix.cs = x.cs;
     sl.ix.dense_nc = x.dense_nc;
     sl.ix.lookup_mode = h->lookup_mode;
-    sl.ix.cont = h->cont;
     {
         uint32_t l = 0;
         while ((1u << l) < x.cs) ++l;  // ceil(log2 cs)
@@ -412,7 +416,11 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
         delete h;
         return fail(EAT_EINVAL, "continuation must be 0 (default), 1 (on) or 2 (off)");
     }
-    h->cont = o.continuation == 1 ? 1u : 0u;  // default off (tools/sweep_cont.py: fewer sweeps, slower)  // default uint32 (tools/sweep_cta.py: uint16 gives no gain)
+    if (o.continuation == 1) {  // measured slower and removed
+        delete h;
+        return fail(EAT_EUNSUPPORTED, "warp-local continuation was removed from the CTA kernel");
+    }
+    if (const char *dv = getenv("EAT_E2E_DIRECT")) h->e2e_direct = atoi(dv) != 0;  // A/B (tools/e2e_ab.py)
     h->part_rank = o.part_rank;
     h->part_count = pc;
     h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 && !o.nccl_unique_id;
@@ -537,6 +545,7 @@ eat_status eat_get_stats(const eat_handle *hc, eat_stats *out) {
         CUDA_TRY(cudaMemcpy(&inv, h->d_invalid, 8, cudaMemcpyDeviceToHost));
         h->st.last_sweeps = sw;
         h->st.invalid_queries = inv;
+        h->st.cta_grid = uint32_t(h->cta_grid);
         if (h->kernel == EAT_KERNEL_ASYNC && h->mode != EAT_MODE_EDGE_PARTITIONED) {
             uint32_t rr = 0;
             CUDA_TRY(cudaMemcpy(&rr, h->d_rounds1, 4, cudaMemcpyDeviceToHost));
@@ -769,6 +778,32 @@ eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t
     cudaPointerAttributes pa{};
     const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
     cudaGetLastError();
+    if (pinned && pa.devicePointer && h->cta_grid > 0 && h->e2e_direct) {
+        // Direct: one persistent launch over all queries; each CTA stores its
+        // finished rows into the page-locked host buffer over PCIe (mapped
+        // pointer), so the D2H traffic overlaps the relaxation of the other
+        // queries with no chunk head/tail.
+        if (!h->bstream[0])
+            for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&h->bstream[i], cudaStreamNonBlocking));
+        if (!h->d_bcounter) CUDA_TRY(cudaMalloc(&h->d_bcounter, 2 * sizeof(unsigned long long)));
+        if (h->dcap < nq) {
+            if (h->d_dsrc) cudaFree(h->d_dsrc);
+            if (h->d_dts) cudaFree(h->d_dts);
+            h->d_dsrc = h->d_dts = nullptr;
+            h->dcap = 0;
+            CUDA_TRY(cudaMalloc(&h->d_dsrc, nq * 4));
+            CUDA_TRY(cudaMalloc(&h->d_dts, nq * 4));
+            h->dcap = nq;
+        }
+        cudaStream_t st = h->bstream[0];
+        CUDA_TRY(cudaMemcpyAsync(h->d_dsrc, sources, nq * 4, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(h->d_dts, times, nq * 4, cudaMemcpyHostToDevice, st));
+        eat_status e = enqueue_batch(h, h->d_dsrc, h->d_dts, nq, static_cast<uint32_t *>(pa.devicePointer), st,
+                                     h->d_bcounter, 1);
+        if (e != EAT_OK) return e;
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return EAT_OK;
+    }
     const uint64_t chunk =
         std::max<uint64_t>(1, std::min<uint64_t>(nq, std::min<uint64_t>(1024, (256ull << 20) / (4 * n))));
     if (!h->bstream[0])

@@ -57,13 +57,13 @@ __global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *boun
 // once; a vertex lowered after it was read is re-marked).
 // Queries are taken dynamically from a global counter (persistent grid).
 //
-// One sweep (three CTA barriers):
+// One sweep (two CTA barriers):
 //   1. select + compact: every thread scans its bitmap words; an active
 //      vertex is selected when e[u] <= base + window (window = EAT_INF: all
 //      of them, the paper's schedule; base = min e[] over the frontier,
 //      tracked incrementally); selected vertices are appended to s_list by
 //      shared-memory atomics (order is irrelevant), the rest stay active;
-//   2. warp-level flattening: each warp takes 32 listed vertices, scans their
+//   2. warp-level flattening: each warp takes g <= 32 listed vertices, scans their
 //      type counts with shuffles and evaluates the (vertex, type) pairs 32 at
 //      a time (owner lane found by a 5-step shuffle search) -- all lanes busy,
 //      no per-vertex divergence, no block scan;
@@ -75,7 +75,10 @@ __global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *boun
 // COUNT: instrumented variant (EAT_BUILD_COUNTERS) accumulating, per launch,
 // the work counters used for algorithmic-byte accounting:
 // counters[0] vertex visits, [1] type records read, [2] cluster records read,
-// [3] spilled items read, [4] improvements (successful atomicMin), [5] sweeps.
+// [3] spilled items read, [4] improvements (successful atomicMin), [5] sweeps,
+// [6]/[7] select / pair phase cycles (thread 0, barrier to barrier), [8]/[9]
+// the slowest warp's own select / pair loop cycles.
+//
 // Shared-memory e[] of one query.  SArr<false>: uint32 arrival times.
 // SArr<true>: uint16 offsets from t_s (0xFFFF = unreached), half the shared
 // memory per query so more queries fit per SM; an improvement whose offset
@@ -132,8 +135,6 @@ struct SArr<true> {
 template <int T, bool A16>
 constexpr int cta_min_blocks() { return T >= 1024 ? 1 : (A16 ? 8 : (T >= 512 ? 4 : 5)); }
 
-constexpr uint32_t kLocalQ = 16;
-
 template <bool COUNT, int kCtaThreads, int kListCap, bool A16, bool TGT>
 __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>())) k_query_cta(DevIndex ix, const uint32_t *__restrict__ src,
                                                                const uint32_t *__restrict__ tsv, uint64_t nq,
@@ -156,7 +157,6 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
     uint32_t *bmD = sm + SArr<A16>::bytes(n) / 4u;  // deferred: active, not yet selected
     uint32_t *bmN = bmD + W;    // new: lowered since their last selection
     __shared__ uint32_t s_list[kListCap];
-    __shared__ uint32_t s_lq[kCtaWarps * kLocalQ];  // warp-local continuation queues
     __shared__ uint32_t s_cnt[2], s_more[2];  // per sweep parity: listed / (deferred + improved)
     __shared__ uint32_t s_tmin[3];            // window base, rotating per sweep
     __shared__ uint32_t s_ovf;                // A16: an arrival offset overflowed
@@ -230,61 +230,45 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             // goal-directed: a vertex with e[u] >= e[dst] cannot lower e[dst]
             const uint32_t best = TGT ? ar.get(di) : uint32_t(kInf);
             const unsigned long long t_sw0 = COUNT ? clock64() : 0ull;
-            // ---- 1. select + compact: active = deferred | new.  The word loop is
-            // warp-uniform so that list slots are allocated with one shared
-            // atomic per warp (warp prefix sum of the selected-bit counts).
+            // ---- 1. select + compact: active = deferred | new
             uint32_t dmin = kInf, ndef = 0;
-            for (uint32_t w0 = 0; w0 < W; w0 += kCtaThreads) {
-                const uint32_t w = w0 + tid;
-                uint32_t word = w < W ? (bmD[w] | bmN[w]) : 0u;
+            for (uint32_t w = tid; w < W; w += kCtaThreads) {
+                uint32_t word = bmD[w] | bmN[w];
+                if (!word) continue;
+                bmN[w] = 0;
                 uint32_t sel = word;
-                if (word) {
-                    bmN[w] = 0;
-                    if (thr < kInf || (TGT && best < kInf)) {
-                        sel = 0;
-                        uint32_t rest = word;
-                        while (rest) {
-                            const uint32_t b = __ffs(rest) - 1u;
-                            rest &= rest - 1u;
-                            const uint32_t a = ar.get(w * 32u + b);
-                            if (TGT && a >= best) word &= ~(1u << b);  // pruned for good
-                            else if (a <= thr) sel |= 1u << b;
-                            else dmin = min(dmin, a);
-                        }
+                if (thr < kInf || (TGT && best < kInf)) {
+                    sel = 0;
+                    uint32_t rest = word;
+                    while (rest) {
+                        const uint32_t b = __ffs(rest) - 1u;
+                        rest &= rest - 1u;
+                        const uint32_t a = ar.get(w * 32u + b);
+                        if (TGT && a >= best) word &= ~(1u << b);  // pruned for good
+                        else if (a <= thr) sel |= 1u << b;
+                        else dmin = min(dmin, a);
                     }
                 }
+                uint32_t taken = 0;
                 const uint32_t k = __popc(sel);
-                uint32_t incl = k;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                    if (lane >= uint32_t(o)) incl += y;
-                }
-                const uint32_t wtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-                uint32_t wbase = 0;
-                if (lane == 0 && wtot) wbase = atomicAdd(&s_cnt[p], wtot);
-                wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
-                if (word) {
-                    uint32_t taken = 0;
-                    if (k) {
-                        const uint32_t pos = wbase + incl - k;
-                        const uint32_t put = pos < uint32_t(kListCap) ? min(k, uint32_t(kListCap) - pos) : 0u;
-                        uint32_t rest = sel;
-                        for (uint32_t i = 0; i < put; ++i) {
-                            const uint32_t b = __ffs(rest) - 1u;
-                            rest &= rest - 1u;
-                            s_list[pos + i] = w * 32u + b;
-                            taken |= 1u << b;
-                        }
-                        while (rest) {  // list full: stays active for a later sweep
-                            const uint32_t b = __ffs(rest) - 1u;
-                            rest &= rest - 1u;
-                            dmin = min(dmin, ar.get(w * 32u + b));
-                        }
+                if (k) {
+                    const uint32_t pos = atomicAdd(&s_cnt[p], k);
+                    const uint32_t put = pos < uint32_t(kListCap) ? min(k, uint32_t(kListCap) - pos) : 0u;
+                    uint32_t rest = sel;
+                    for (uint32_t i = 0; i < put; ++i) {
+                        const uint32_t b = __ffs(rest) - 1u;
+                        rest &= rest - 1u;
+                        s_list[pos + i] = w * 32u + b;
+                        taken |= 1u << b;
                     }
-                    bmD[w] = word & ~taken;
-                    ndef += __popc(word & ~taken);
+                    while (rest) {  // list full: stays active for a later sweep
+                        const uint32_t b = __ffs(rest) - 1u;
+                        rest &= rest - 1u;
+                        dmin = min(dmin, ar.get(w * 32u + b));
+                    }
                 }
+                bmD[w] = word & ~taken;
+                ndef += __popc(word & ~taken);
             }
             if (COUNT && lane == 0) atomicMax(&s_tw[0], clock64() - t_sw0);
             if (window < kInf) {
@@ -310,41 +294,14 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             const uint32_t F = min(s_cnt[p], uint32_t(kListCap));
             // ---- 2. warp-level flattened (vertex, type) pairs; a warp takes g
             // consecutive list entries so that small frontiers still spread
-            // over all warps.  Continuation (ix.cont): a vertex the warp lowers
-            // within the current window goes to a small warp-local queue and is
-            // relaxed by the same warp in this sweep (claimed by clearing its
-            // new-bit), so a chain of improvements advances several hops per
-            // sweep instead of one.
+            // over all warps
             const uint32_t g = min(32u, max(1u, (F + kCtaWarps - 1u) / kCtaWarps));
-            uint32_t nimpr = 0, cmin = kInf;
-            uint32_t k0 = wid * g;
-            uint32_t lq_cnt = 0;  // warp-uniform
-            uint32_t *lq = s_lq + wid * kLocalQ;
-            for (;;) {
+            uint32_t nimpr = 0;
+            for (uint32_t k0 = wid * g; k0 < F; k0 += kCtaWarps * g) {
+                const uint32_t j = k0 + lane;
                 uint32_t x = 0, p0 = 0, nt = 0;
-                bool valid = false;
-                if (k0 < F) {
-                    const uint32_t j = k0 + lane;
-                    valid = lane < g && j < F;
-                    if (valid) x = s_list[j];
-                    k0 += kCtaWarps * g;
-                } else if (lq_cnt > 0) {
-                    const uint32_t take = min(lq_cnt, 32u);
-                    if (lane < take) {
-                        x = lq[lq_cnt - take + lane];
-                        const uint32_t bit = 1u << (x & 31u);
-                        valid = (atomicAnd(bmN + (x >> 5), ~bit) & bit) != 0u;  // claim
-                        if (valid && thr < kInf && ar.get(x) > thr) {  // left the window: next sweeps
-                            atomicOr(bmN + (x >> 5), bit);
-                            valid = false;
-                        }
-                    }
-                    lq_cnt -= take;
-                    __syncwarp();
-                } else {
-                    break;
-                }
-                if (valid) {
+                if (lane < g && j < F) {
+                    x = s_list[j];
                     p0 = __ldg(ix.type_ptr + x);
                     nt = __ldg(ix.type_ptr + x + 1) - p0;
                     if (COUNT) ++c_vis;
@@ -369,61 +326,44 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
                     const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
                     const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
-                    uint32_t pushv = kNone;
-                    do {
-                        if (qp >= tot) break;
-                        const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
-                        const uint32_t eu = ar.get(u);
-                        CrecPrefetch pf{};
-                        if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the type record
-                        const TypeRec tr = load_type(ix, t);
-                        if (COUNT) ++c_type;
-                        if (eu > tr.last) break;
-                        const uint32_t av = ar.get(tr.v);
-                        const uint32_t lim = TGT ? min(av, ar.get(di)) : av;
-                        if (max(eu, tr.first) + tr.lam >= lim) break;  // PAPER.md:411-416 (+ target bound)
-                        uint32_t tc;
-                        if (eu <= tr.first) {
-                            tc = tr.first;
-                        } else {
-                            tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
-                                             : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
-                            if (COUNT) {
-                                ++c_crec;
-                                const uint4 rr = __ldg(ix.crec + 2ull * (tr.crec_base + cluster_of(ix, eu) - tr.c_first));
-                                if (rr.y == kItemSpill) c_spill += rr.w;
-                            }
+                    if (qp >= tot) continue;
+                    const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
+                    const uint32_t eu = ar.get(u);
+                    CrecPrefetch pf{};
+                    if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the type record
+                    const TypeRec tr = load_type(ix, t);
+                    if (COUNT) ++c_type;
+                    if (eu > tr.last) continue;
+                    const uint32_t av = ar.get(tr.v);
+                    const uint32_t lim = TGT ? min(av, ar.get(di)) : av;
+                    if (max(eu, tr.first) + tr.lam >= lim) continue;  // PAPER.md:411-416 (+ target bound)
+                    uint32_t tc;
+                    if (eu <= tr.first) {
+                        tc = tr.first;
+                    } else {
+                        tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
+                                         : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                        if (COUNT) {
+                            ++c_crec;
+                            const uint4 rr = __ldg(ix.crec + 2ull * (tr.crec_base + cluster_of(ix, eu) - tr.c_first));
+                            if (rr.y == kItemSpill) c_spill += rr.w;
                         }
-                        const uint32_t cand = tc + tr.lam;
-                        if (cand < av) {
-                            const uint32_t old = ar.amin(tr.v, cand, &s_ovf);
-                            if (cand < old) {
-                                atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
-                                cmin = min(cmin, cand);
-                                ++nimpr;
-                                if (COUNT) ++c_impr;
-                                if (cand <= thr) pushv = tr.v;
-                            }
+                    }
+                    const uint32_t cand = tc + tr.lam;
+                    if (cand < av) {
+                        const uint32_t old = ar.amin(tr.v, cand, &s_ovf);
+                        if (cand < old) {
+                            atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
+                            if (window < kInf) atomicMin(&s_tmin[t_nxt], cand);
+                            ++nimpr;
+                            if (COUNT) ++c_impr;
                         }
-                    } while (0);
-                    if (ix.cont) {  // append this round's improvements to the warp-local queue
-                        const unsigned m = __ballot_sync(0xFFFFFFFFu, pushv != kNone);
-                        if (m) {
-                            const uint32_t pos = lq_cnt + __popc(m & ((1u << lane) - 1u));
-                            if (pushv != kNone && pos < kLocalQ) lq[pos] = pushv;
-                            lq_cnt = min(uint32_t(kLocalQ), lq_cnt + uint32_t(__popc(m)));
-                        }
-                        __syncwarp();
                     }
                 }
             }
             if (COUNT && lane == 0) atomicMax(&s_tw[1], clock64() - t_pr0);
             nimpr = __reduce_add_sync(0xFFFFFFFFu, nimpr);
             if (lane == 0 && nimpr) atomicAdd(&s_more[p], nimpr);
-            if (window < kInf) {  // window base of the next sweep: one shared atomic per warp
-                cmin = __reduce_min_sync(0xFFFFFFFFu, cmin);
-                if (lane == 0 && cmin < kInf) atomicMin(&s_tmin[t_nxt], cmin);
-            }
             __syncthreads();
             if (COUNT && tid == 0) {
                 const unsigned long long now = clock64();
@@ -444,6 +384,14 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
         // Output in caller ids
         if (TGT) {
             if (tid == 0) orow[0] = ar.get(di);
+        } else if ((n & 3u) == 0u && (reinterpret_cast<uintptr_t>(orow) & 15u) == 0u) {
+            // 16-byte stores (rows may live in mapped host memory: eat_query_many direct mode)
+            const uint4 *pv = reinterpret_cast<const uint4 *>(ix.perm);
+            uint4 *ov = reinterpret_cast<uint4 *>(orow);
+            for (uint32_t i = tid; i < n / 4u; i += kCtaThreads) {
+                const uint4 pi = __ldg(pv + i);
+                ov[i] = make_uint4(ar.get(pi.x), ar.get(pi.y), ar.get(pi.z), ar.get(pi.w));
+            }
         } else {
             for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = ar.get(__ldg(ix.perm + i));
         }

@@ -1,0 +1,24 @@
+"""Time the city batch (10k queries, device buffers) with a given libeat.so
+build (A/B of kernel versions on one box).  Usage: python tools/ab_lib.py path/to/libeat.so"""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch, synth
+from paper_1912_00966_b200 import _lib
+_lib.LIB_PATH = os.path.abspath(sys.argv[1])
+from paper_1912_00966_b200 import Engine
+tt = synth.generate("city")
+src, ts = synth.queries(tt, 1000, 10)
+d_src = torch.tensor(src.astype(np.int32), device="cuda")
+d_ts = torch.tensor(ts.astype(np.int32), device="cuda")
+out = torch.empty((src.size, tt.num_vertices), dtype=torch.int32, device="cuda")
+eng = Engine.from_timetable(tt, subtrips=2)
+for _ in range(3):
+    eng.query_many_device(d_src, d_ts, out)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ms = []
+for _ in range(7):
+    a.record(); eng.query_many_device(d_src, d_ts, out); b.record(); b.synchronize()
+    ms.append(a.elapsed_time(b))
+print(json.dumps({"lib": os.path.basename(sys.argv[1]), "batch_ms_med": float(np.median(ms)), "qps": src.size / float(np.median(ms)) * 1e3,
+                  "crc": int(out[::97].sum().item())}), flush=True)
