@@ -363,8 +363,10 @@ def run_gpu(args):
         eng0.close()
 
     # ---- e2e through the public API with host buffers: pinned host queries
-    # in, every step H2D of the queries + kernel + D2H of all result rows into
-    # pinned host memory (eat_query_many pipelines chunks over two streams)
+    # in, every step H2D of the queries + kernel + all result rows to pinned
+    # host memory (eat_query_many "direct" mode: each CTA stores its finished
+    # rows into the mapped host buffer over PCIe, overlapped with the other
+    # queries' relaxation; pageable buffers go through a two-stream pipeline)
     from paper_1912_00966_b200 import pinned_empty
 
     h_out = pinned_empty((nq, tt.num_vertices))

@@ -138,10 +138,16 @@ typedef struct eat_build_opts {
                                      1 dense (record of type t, cluster k at t*y + k -- the paper's CL[y*i+j],
                                      PAPER.md:386-390: fetched in parallel with the type record),
                                      2 compact (records only for [c_first, c_last] of each type) */
-    uint32_t continuation;        /* 0 or 2.  1 (warp-local continuation of improvements inside a sweep) was
-                                     an experiment of round 1, measured slower and removed: EAT_EUNSUPPORTED. */
+    uint32_t continuation;        /* grid frontier kernel (single queries whose e[] does not fit one CTA):
+                                     after a sub-warp lowers e[v] it relaxes v's types itself in the same
+                                     sweep, up to this many extra vertices per frontier vertex, so a chain
+                                     advances several hops per sweep (measured: metro -11 %, country -15 %
+                                     at 1; deeper chains lengthen the slowest sweep).  0 = default (1),
+                                     EAT_CONT_NONE = off (one hop per sweep, the paper's schedule),
+                                     1..64 explicit; else EAT_EINVAL. */
 } eat_build_opts;
 
+#define EAT_CONT_NONE 0xFFFFFFFFu
 #define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */
 
 typedef struct eat_handle eat_handle;

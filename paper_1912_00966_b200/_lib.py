@@ -13,6 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libeat.so")
 
 EAT_INF = 0x7FFFFFFF
+EAT_CONT_NONE = 0xFFFFFFFF  # eat_build_opts.continuation: no continuation (one hop per sweep)
 
 EAT_OK, EAT_EINVAL, EAT_ERANGE, EAT_ENOMEM, EAT_ECUDA, EAT_ENCCL, EAT_EUNSUPPORTED, EAT_ESTATE = range(8)
 STATUS_NAMES = ["EAT_OK", "EAT_EINVAL", "EAT_ERANGE", "EAT_ENOMEM", "EAT_ECUDA", "EAT_ENCCL",

@@ -77,6 +77,7 @@ struct eat_handle {
     uint32_t window = EAT_INF;           // CTA schedule time window (EAT_INF = all active vertices)
     uint32_t cta_threads = 256;          // CTA-kernel variant (batched queries)
     uint32_t lookup_mode = 0;            // 0 Cluster-AP; NEXT-3 ablations 1 (Connection-type-AP), 2 (linear)
+    uint32_t cont_budget = 1;            // grid frontier kernel: continuation hops per frontier vertex
     std::vector<uint4> raw;              // EAT_KERNEL_CONNECTION: raw connections until upload
     uint4 *d_conns = nullptr;
     bool arr16 = true;                   // batched CTA kernel keeps e[] as uint16 offsets (+ uint32 recompute)
@@ -194,6 +195,7 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     sl.ix.cs = x.cs;
     sl.ix.dense_nc = x.dense_nc;
     sl.ix.lookup_mode = h->lookup_mode;
+    sl.ix.cont_budget = h->cont_budget;
     {
         uint32_t l = 0;
         while ((1u << l) < x.cs) ++l;  // ceil(log2 cs)
@@ -412,14 +414,11 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
         return fail(EAT_EINVAL, "arr_bits must be 0, 16 or 32");
     }
     h->arr16 = o.arr_bits == 16;
-    if (o.continuation > 2) {
+    if (o.continuation != EAT_CONT_NONE && o.continuation > 64) {
         delete h;
-        return fail(EAT_EINVAL, "continuation must be 0 (default), 1 (on) or 2 (off)");
+        return fail(EAT_EINVAL, "continuation must be 0 (default 1), 1..64 or EAT_CONT_NONE");
     }
-    if (o.continuation == 1) {  // measured slower and removed
-        delete h;
-        return fail(EAT_EUNSUPPORTED, "warp-local continuation was removed from the CTA kernel");
-    }
+    h->cont_budget = o.continuation == 0 ? 1u : (o.continuation == EAT_CONT_NONE ? 0u : o.continuation);
     if (const char *dv = getenv("EAT_E2E_DIRECT")) h->e2e_direct = atoi(dv) != 0;  // A/B (tools/e2e_ab.py)
     h->part_rank = o.part_rank;
     h->part_count = pc;

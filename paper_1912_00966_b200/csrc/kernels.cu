@@ -532,14 +532,35 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
             const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
             uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
             const uint32_t lane = uint32_t(gtid % SW);
+            // continuation: a sub-warp that lowers e[v] relaxes v's types itself
+            // in this sweep (up to ix.cont_budget extra vertices per frontier
+            // vertex, default 1) instead of queueing v for the next sweep: a
+            // chain advances up to 1 + budget hops per sweep.  v is not stamped,
+            // so a later lowering by anyone still queues it (chaotic relaxation
+            // converges to the same fixpoint)
+            const uint32_t wl = threadIdx.x & 31u;
+            const unsigned smask = SW == 32 ? 0xFFFFFFFFu : (((1u << SW) - 1u) << (wl & ~(SW - 1u)));
             for (uint64_t it = gtid / SW; it < cnt; it += gsz / SW) {
-                const uint32_t x = ld_cg(qc + it);
-                const uint32_t eu = ld_cg(w.arr + x);
-                const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
-                for (uint32_t t = p0 + lane; t < p1; t += SW) {
-                    const uint32_t v = relax_type_global(ix, t, eu, w.arr);
-                    if (v != kNone && atomicExch(w.stamp + v, sweep + 1u) != sweep + 1u)
-                        push_aggregated(v, qn, w.ctl + c_nxt);
+                uint32_t x = ld_cg(qc + it);
+                uint32_t budget = ix.cont_budget;
+                for (;;) {
+                    const uint32_t eu = ld_cg(w.arr + x);
+                    const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
+                    uint32_t cv = kNone;
+                    for (uint32_t t = p0 + lane; t < p1; t += SW) {
+                        const uint32_t v = relax_type_global(ix, t, eu, w.arr);
+                        if (v == kNone) continue;
+                        if (budget > 0 && cv == kNone) cv = v;
+                        else if (atomicExch(w.stamp + v, sweep + 1u) != sweep + 1u) push_aggregated(v, qn, w.ctl + c_nxt);
+                    }
+                    const unsigned cm = __ballot_sync(smask, cv != kNone) & smask;
+                    if (!cm) break;
+                    const uint32_t src = __ffs(cm) - 1u;
+                    const uint32_t nx = __shfl_sync(smask, cv, src);
+                    if (cv != kNone && wl != src && atomicExch(w.stamp + cv, sweep + 1u) != sweep + 1u)
+                        push_aggregated(cv, qn, w.ctl + c_nxt);
+                    x = nx;
+                    --budget;
                 }
             }
         } else {

@@ -15,6 +15,7 @@ struct DevIndex {
     uint32_t cs_shift;          // 31 + l   (exact for every e < 2^31)
     uint32_t dense_nc;          // > 0: dense cluster directory, record (t, k) at t*dense_nc + k
     uint32_t lookup_mode;       // 0 Cluster-AP; ablations (grid kernels): 1 Connection-type-AP, 2 Connection-type linear
+    uint32_t cont_budget;       // grid frontier kernel: extra vertices a sub-warp relaxes in the same sweep (continuation)
     uint64_t num_conns;         // connection-version schedule: raw connections on the device
     const uint4 *conns;         // [num_conns] {u, v, dep, arr} internal ids (EAT_KERNEL_CONNECTION only)
     uint64_t num_types;

@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
     bool remote = false;
     uint32_t sweep = 0;
     const uint32_t lane = uint32_t(gtid % SW);
+    const uint32_t wl = threadIdx.x & 31u;
+    const unsigned smask = SW == 32 ? 0xFFFFFFFFu : (((1u << SW) - 1u) << (wl & ~(SW - 1u)));
     for (;;) {
         const uint32_t c_cur = sweep % 3u, c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
         if (gtid == 0) w.ctl[c_old] = 0;
@@ -64,18 +66,34 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
         const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
         uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
         const uint32_t stamp = base + sweep + 1u;
+        // continuation as in the grid frontier kernel (kernels.cu): an owned
+        // vertex lowered by this sub-warp is relaxed by it in the same sweep
+        // (up to ix.cont_budget extra vertices per frontier vertex)
         for (uint64_t it = gtid / SW; it < cnt; it += gsz / SW) {
-            const uint32_t x = ld_cg(qc + it);
-            const uint32_t eu = ld_cg(w.arr + x);
-            const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
-            for (uint32_t t = p0 + lane; t < p1; t += SW) {
-                const uint32_t v = relax_type_global(ix, t, eu, w.arr);
-                if (v == kNone) continue;
-                if (v >= lo && v < hi) {
-                    if (atomicExch(w.stamp + v, stamp) != stamp) push_aggregated(v, qn, w.ctl + c_nxt);
-                } else {
-                    remote = true;
+            uint32_t x = ld_cg(qc + it);
+            uint32_t budget = ix.cont_budget;
+            for (;;) {
+                const uint32_t eu = ld_cg(w.arr + x);
+                const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
+                uint32_t cv = kNone;
+                for (uint32_t t = p0 + lane; t < p1; t += SW) {
+                    const uint32_t v = relax_type_global(ix, t, eu, w.arr);
+                    if (v == kNone) continue;
+                    if (v >= lo && v < hi) {
+                        if (budget > 0 && cv == kNone) cv = v;
+                        else if (atomicExch(w.stamp + v, stamp) != stamp) push_aggregated(v, qn, w.ctl + c_nxt);
+                    } else {
+                        remote = true;
+                    }
                 }
+                const unsigned cm = __ballot_sync(smask, cv != kNone) & smask;
+                if (!cm) break;
+                const uint32_t src = __ffs(cm) - 1u;
+                const uint32_t nx = __shfl_sync(smask, cv, src);
+                if (cv != kNone && wl != src && atomicExch(w.stamp + cv, stamp) != stamp)
+                    push_aggregated(cv, qn, w.ctl + c_nxt);
+                x = nx;
+                --budget;
             }
         }
         grid_sync(bar);

@@ -48,7 +48,7 @@ class Engine:
                  host_only: bool = False, counters: bool = False, mode: str = "replicated", part_rank: int = 0, part_count: int = 1,
                  nccl_unique_id: Optional[bytes] = None, window: int = 0,
                  cta_threads: int = 0, subtrips: int = 0, trip=None, arr_bits: int = 0,
-                 cluster_dir: str = "auto", lookup: str = "cluster_ap", continuation: bool = False):
+                 cluster_dir: str = "auto", lookup: str = "cluster_ap", continuation: Optional[int] = None):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
@@ -74,7 +74,7 @@ class Engine:
                                    subtrips=int(subtrips), arr_bits=int(arr_bits),
                                    cluster_dir={"auto": 0, "dense": 1, "compact": 2}[cluster_dir],
                                    lookup={"cluster_ap": 0, "ap": 1, "linear": 2}[lookup],
-                                   continuation=1 if continuation else 2)
+                                   continuation=0 if continuation is None else (int(continuation) or _lib.EAT_CONT_NONE))
         self._h = _lib.eat_build(tt, opts)
         self.num_vertices = int(num_vertices)
         self.num_connections = int(m)

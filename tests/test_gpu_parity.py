@@ -98,7 +98,8 @@ def test_random_small_instances(kernel):
         eng = Engine.from_timetable(tt, kernel=kernel, cluster_seconds=[3600, 600, 4096, 60][seed % 4],
                                     subwarp=[1, 2, 4, 8, 16, 32, 0, 64][seed % 8],
                                     cta_threads=[256, 384, 512, 192, 128][seed % 5], arr_bits=[16, 32][seed % 2],
-                                    cluster_dir=["auto", "dense", "compact"][seed % 3])
+                                    cluster_dir=["auto", "dense", "compact"][seed % 3],
+                                    continuation=[None, 0, 2, 4, 64, 1, 16][seed % 7])
         csa = oracle.CSA(tt.num_vertices, *tt.arrays())
         rng = np.random.default_rng(seed)
         for _ in range(3):

@@ -20,5 +20,12 @@ ms = []
 for _ in range(7):
     a.record(); eng.query_many_device(d_src, d_ts, out); b.record(); b.synchronize()
     ms.append(a.elapsed_time(b))
+o1 = torch.empty(tt.num_vertices, dtype=torch.int32, device="cuda")
+for _ in range(3):
+    eng.query_device(*synth.SINGLE_QUERY, o1)
+a.record()
+for _ in range(20):
+    eng.query_device(*synth.SINGLE_QUERY, o1)
+b.record(); b.synchronize()
 print(json.dumps({"lib": os.path.basename(sys.argv[1]), "batch_ms_med": float(np.median(ms)), "qps": src.size / float(np.median(ms)) * 1e3,
-                  "crc": int(out[::97].sum().item())}), flush=True)
+                  "single_ms": a.elapsed_time(b) / 20, "crc": int(out[::97].sum().item()), "crc1": int(o1.sum().item())}), flush=True)
