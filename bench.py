@@ -45,6 +45,40 @@ def _dist():
     return rank, world, local
 
 
+def _init_dist():
+    """One process per GPU (torchrun env); rank r drives GPU LOCAL_RANK.
+    EAT_BENCH_BACKEND=gloo (with more ranks than GPUs, ranks share devices
+    round-robin) exercises the multi-rank logic on a one-GPU box."""
+    import torch
+
+    rank, world, local = _dist()
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        backend = os.environ.get("EAT_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    return rank, world, dev
+
+
+def _max_over_ranks(x: float, dev: int) -> float:
+    """Max of a host float over all ranks (device tensor under NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        return x
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -183,15 +217,7 @@ def run_single(args):
     """Single-query latency workloads (metric: EAT single-query ms)."""
     import torch
 
-    rank, world, local = _dist()
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.cuda.current_device()
+    rank, world, dev = _init_dist()
     import synth
     from paper_1912_00966_b200 import Engine
     from paper_1912_00966_b200.parallel import nccl_unique_id
@@ -231,10 +257,7 @@ def run_single(args):
     clk = clocks.stop()
     ms = [a.elapsed_time(b) for a, b in ev]
     tot = float(sum(ms))
-    if world > 1:
-        t = torch.tensor([tot], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot = float(t.item())
+    tot = _max_over_ranks(tot, dev)
     st = eng.stats()
     # e2e: public host API (D2H of e[] included)
     h = None
@@ -283,15 +306,7 @@ def run_single(args):
 def run_gpu(args):
     import torch
 
-    rank, world, local = _dist()
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.cuda.current_device()
+    rank, world, dev = _init_dist()
     import synth
     from paper_1912_00966_b200 import Engine
 
@@ -337,10 +352,7 @@ def run_gpu(args):
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = float(sum(step_ms))
-    if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot_ms = _max_over_ranks(tot_ms, dev)
     value = world * nq * args.steps / (tot_ms / 1e3)
 
     # ---- the same batch without sub-trip shortcuts (plain Cluster-AP index)
@@ -382,10 +394,7 @@ def run_gpu(args):
         eng.query_many(h_src, h_ts, out=h_out)
     e2e_s = time.perf_counter() - t0
     e2e_ok = bool(np.array_equal(h_out[:64].view(np.int32), d_out[:64].cpu().numpy()))
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = _max_over_ranks(e2e_s, dev)
     e2e_value = world * nq * e2e_steps / e2e_s
 
     # ---- single-query latency (BASELINE configs[1]: s=0, t_s=06:00)
