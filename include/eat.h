@@ -104,6 +104,17 @@ enum {
 /* eat_build_opts.flags */
 #define EAT_BUILD_HOST_ONLY 0x1u   /* compress only, no device upload: introspection (eat_index_*) */
 #define EAT_BUILD_COUNTERS 0x2u    /* batched kernel runs its instrumented variant (work counters in eat_stats) */
+#define EAT_BUILD_MULTIPROCESS 0x4u /* EDGE_PARTITIONED + EAT_EXCHANGE_PEER: this process is rank part_rank of
+                                       part_count processes (blocks joined with eat_peer_export/connect);
+                                       without it all part_count partitions run in this process (loopback) */
+
+/* eat_build_opts.exchange (EDGE_PARTITIONED): how partitions share e[] */
+#define EAT_EXCHANGE_ALLREDUCE 0u  /* host-driven rounds: local sweeps, then ncclAllReduce(min) of e[] ++ flag */
+#define EAT_EXCHANGE_PEER 1u       /* in-kernel (NEXT-2): a lowered vertex owned elsewhere gets a system-scope
+                                      atomicMin on its owner's e[] through a peer pointer plus an inbox entry;
+                                      cross-partition barrier in device memory; no host round trip, no dense
+                                      collective.  Loopback: all partitions as CTA groups of one launch. */
+#define EAT_PEER_HANDLE_BYTES 64u  /* one rank's exported exchange-block handle (cudaIpcMemHandle_t) */
 
 typedef struct eat_build_opts {
     uint32_t cluster_seconds;     /* hour-cluster width; 0 -> 3600; valid 1..4096 */
@@ -145,6 +156,7 @@ typedef struct eat_build_opts {
                                      at 1; deeper chains lengthen the slowest sweep).  0 = default (1),
                                      EAT_CONT_NONE = off (one hop per sweep, the paper's schedule),
                                      1..64 explicit; else EAT_EINVAL. */
+    uint32_t exchange;            /* EDGE_PARTITIONED: EAT_EXCHANGE_ALLREDUCE (default) or EAT_EXCHANGE_PEER */
 } eat_build_opts;
 
 #define EAT_CONT_NONE 0xFFFFFFFFu
@@ -269,6 +281,19 @@ eat_status eat_index_export(const eat_handle *h, uint32_t *perm, uint32_t *type_
  * pointer may be NULL.  Errors: EAT_EINVAL for a NULL handle. */
 eat_status eat_index_sizes(const eat_handle *h, uint64_t *num_types, uint64_t *num_cluster_records,
                            uint64_t *num_pool_items);
+
+/* EAT_EXCHANGE_PEER across processes (one per GPU), collective in this order:
+ * every rank builds with EAT_BUILD_MULTIPROCESS, exports its exchange-block
+ * handle (EAT_PEER_HANDLE_BYTES into handle_out), the caller all-gathers the
+ * handles in rank order (e.g. torch.distributed), every rank connects with
+ * the part_count handles (its own entry is ignored).  The blocks are mapped
+ * with cudaIpcOpenMemHandle (NVLink peer access between GPUs; also works for
+ * two processes on one device).  Queries are then collective like NCCL's:
+ * every rank calls eat_query/eat_query_device with the same (s, t_s) and gets
+ * the full e[].  Errors: EAT_ESTATE on a handle of another kind or a second
+ * connect, EAT_EINVAL on count != part_count, EAT_ECUDA on IPC failures. */
+eat_status eat_peer_export(eat_handle *h, void *handle_out);
+eat_status eat_peer_connect(eat_handle *h, const void *handles, uint32_t count);
 
 /* Internal-vertex range [*lo, *hi) whose out-types partition `rank` of
  * `count` owns in EAT_MODE_EDGE_PARTITIONED (contiguous after renumbering,

@@ -25,11 +25,14 @@ EAT_KERNEL_NAMES = {v: k for k, v in EAT_KERNEL.items()}
 EAT_MODE = {"replicated": 0, "edge_partitioned": 1}
 EAT_BUILD_HOST_ONLY = 0x1
 EAT_BUILD_COUNTERS = 0x2
+EAT_BUILD_MULTIPROCESS = 0x4
+EAT_EXCHANGE = {"allreduce": 0, "peer": 1}
+EAT_PEER_HANDLE_BYTES = 64
 
 # symbols include/eat.h declares (checked by tests/test_abi.py)
 EXPORTED = ["eat_build", "eat_query", "eat_query_device", "eat_query_many", "eat_query_many_device",
             "eat_query_many_target", "eat_query_many_target_device",
-            "eat_lookup_device", "eat_get_stats", "eat_index_export", "eat_index_sizes", "eat_partition_range", "eat_free", "eat_last_error",
+            "eat_lookup_device", "eat_get_stats", "eat_index_export", "eat_index_sizes", "eat_partition_range", "eat_peer_export", "eat_peer_connect", "eat_free", "eat_last_error",
             "eat_abi_version"]
 
 u32p = ctypes.POINTER(ctypes.c_uint32)
@@ -48,7 +51,7 @@ class eat_build_opts(ctypes.Structure):
                 ("nccl_unique_id", ctypes.c_void_p), ("window_seconds", ctypes.c_uint32),
                 ("cta_threads", ctypes.c_uint32), ("subtrips", ctypes.c_uint32),
                 ("arr_bits", ctypes.c_uint32), ("lookup", ctypes.c_uint32), ("cluster_dir", ctypes.c_uint32),
-                ("continuation", ctypes.c_uint32)]
+                ("continuation", ctypes.c_uint32), ("exchange", ctypes.c_uint32)]
 
 
 class eat_stats(ctypes.Structure):
@@ -117,6 +120,10 @@ def lib() -> ctypes.CDLL:
         L.eat_index_sizes.restype = S
         L.eat_partition_range.argtypes = [H, ctypes.c_uint32, ctypes.c_uint32, u32p, u32p]
         L.eat_partition_range.restype = S
+        L.eat_peer_export.argtypes = [H, ctypes.c_void_p]
+        L.eat_peer_export.restype = S
+        L.eat_peer_connect.argtypes = [H, ctypes.c_void_p, ctypes.c_uint32]
+        L.eat_peer_connect.restype = S
         L.eat_free.argtypes = [H]
         L.eat_free.restype = None
         L.eat_last_error.argtypes = []
@@ -187,6 +194,20 @@ def eat_partition_range(h, rank: int, count: int):
     lo, hi = ctypes.c_uint32(), ctypes.c_uint32()
     check(lib().eat_partition_range(h, rank, count, ctypes.byref(lo), ctypes.byref(hi)))
     return lo.value, hi.value
+
+
+def eat_peer_export(h) -> bytes:
+    buf = ctypes.create_string_buffer(EAT_PEER_HANDLE_BYTES)
+    check(lib().eat_peer_export(h, buf))
+    return buf.raw
+
+
+def eat_peer_connect(h, handles) -> None:
+    blob = b"".join(bytes(x) for x in handles)
+    if len(blob) != EAT_PEER_HANDLE_BYTES * len(handles):
+        raise ValueError("every peer handle must be EAT_PEER_HANDLE_BYTES long")
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    check(lib().eat_peer_connect(h, buf, len(handles)))
 
 
 def eat_free(h):

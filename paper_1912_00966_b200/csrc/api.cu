@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 #include "async.cuh"
 #include "partition.cuh"
+#include "peer.cuh"
 
 namespace {
 
@@ -115,6 +116,17 @@ struct eat_handle {
     // edge partition
     uint32_t part_rank = 0, part_count = 1, part_lo = 0, part_hi = 0;
     ncclComm_t comm = nullptr;
+    // EAT_EXCHANGE_PEER (peer.cu): this process's exchange blocks (all P in
+    // loopback), blocks of other ranks mapped by CUDA IPC, the launch context
+    uint32_t exchange = EAT_EXCHANGE_ALLREDUCE;
+    std::vector<void *> peer_own;     // blocks allocated here
+    std::vector<void *> peer_mapped;  // blocks opened with cudaIpcOpenMemHandle (multi-process)
+    std::vector<eat::PeerLocal> peer_loc;
+    eat::PeerCtx peer_ctx{};
+    eat::PeerCtx *d_peer_ctx = nullptr;
+    eat::DevIndex *d_peer_ix = nullptr;
+    eat::PeerLocal *d_peer_loc = nullptr;
+    bool peer_ready = false;
     // stats
     eat_stats st{};
 };
@@ -144,6 +156,14 @@ void release_device(eat_handle *h) {
         if (h->bstream[i]) cudaStreamDestroy(h->bstream[i]);
     }
     if (h->comm) ncclCommDestroy(h->comm);
+    for (void *p : h->peer_mapped)
+        if (p) cudaIpcCloseMemHandle(p);
+    for (void *p : h->peer_own)
+        if (p) cudaFree(p);
+    for (eat::PeerLocal &l : h->peer_loc) eat::peer_local_free(l);
+    void *pp[] = {h->d_peer_ctx, h->d_peer_ix, h->d_peer_loc};
+    for (void *p : pp)
+        if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
 }
 
@@ -216,6 +236,58 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     return EAT_OK;
 }
 
+// Copy the peer launch context (and, once, the slices' indexes and the local
+// scratch descriptors) to the device.
+eat_status peer_publish(eat_handle *h) {
+    const size_t G = h->slices.size();
+    if (!h->d_peer_ctx) CUDA_TRY(cudaMalloc(&h->d_peer_ctx, sizeof(eat::PeerCtx)));
+    if (!h->d_peer_ix) {
+        std::vector<eat::DevIndex> ixs;
+        for (const Slice &sl : h->slices) ixs.push_back(sl.ix);
+        CUDA_TRY(cudaMalloc(&h->d_peer_ix, G * sizeof(eat::DevIndex)));
+        CUDA_TRY(cudaMemcpy(h->d_peer_ix, ixs.data(), G * sizeof(eat::DevIndex), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&h->d_peer_loc, G * sizeof(eat::PeerLocal)));
+        CUDA_TRY(cudaMemcpy(h->d_peer_loc, h->peer_loc.data(), G * sizeof(eat::PeerLocal), cudaMemcpyHostToDevice));
+    }
+    CUDA_TRY(cudaMemcpy(h->d_peer_ctx, &h->peer_ctx, sizeof(eat::PeerCtx), cudaMemcpyHostToDevice));
+    return EAT_OK;
+}
+
+// EAT_EXCHANGE_PEER: one zeroed exchange block per partition held here (all
+// P in loopback, else this rank's; the others arrive with eat_peer_connect),
+// local frontier scratch, the launch context.
+eat_status peer_setup(eat_handle *h) {
+    const eat::HostIndex &x = h->hx;
+    const uint32_t n = x.n, P = h->part_count;
+    if (P > eat::kMaxPeerParts) return fail(EAT_EINVAL, "EAT_EXCHANGE_PEER supports at most 16 partitions");
+    eat::PeerCtx &c = h->peer_ctx;
+    c = eat::PeerCtx{};
+    c.P = P;
+    c.groups = uint32_t(h->slices.size());
+    c.part0 = h->loopback ? 0u : h->part_rank;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = eat::peer_ctas_per_sm();
+    if (per_sm < 1 || uint32_t(sms * per_sm) < c.groups) return fail(EAT_EUNSUPPORTED, "peer kernel does not fit the device");
+    c.ctas_per_group = uint32_t(sms * per_sm) / c.groups;
+    h->peer_loc.resize(c.groups);
+    for (uint32_t g = 0; g < c.groups; ++g) {
+        const uint32_t p = c.part0 + g;
+        uint32_t lo = 0, hi = 0;
+        eat::partition_range(x, p, P, lo, hi);
+        void *blk = nullptr;
+        CUDA_TRY(cudaMalloc(&blk, eat::peer_block_bytes(n, hi - lo)));
+        h->peer_own.push_back(blk);
+        CUDA_TRY(cudaMemset(blk, 0, eat::peer_block_bytes(n, hi - lo)));
+        c.part[p] = eat::peer_part_view(blk, n, lo, hi);
+        if (p == 0) c.gctl = eat::peer_gctl(blk, n, hi - lo);
+        if (eat::peer_local_alloc(h->peer_loc[g], n) != cudaSuccess) return fail(EAT_ENOMEM, "cannot allocate peer scratch");
+    }
+    h->peer_ready = h->loopback || P == 1;
+    return peer_publish(h);
+}
+
 eat_status upload(eat_handle *h) {
     const eat::HostIndex &x = h->hx;
     const uint32_t n = x.n;
@@ -256,9 +328,10 @@ eat_status upload(eat_handle *h) {
     CUDA_TRY(cudaMalloc(&h->d_counter, 8));
     CUDA_TRY(cudaMalloc(&h->d_invalid, 8));
     CUDA_TRY(cudaMemset(h->d_invalid, 0, 8));
-    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED && h->exchange == EAT_EXCHANGE_ALLREDUCE)
         for (Slice &sl : h->slices)
             if (eat::part_alloc(sl.pw, n) != cudaSuccess) return fail(EAT_ENOMEM, "cannot allocate partition scratch");
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED && h->exchange == EAT_EXCHANGE_PEER) return peer_setup(h);
     return EAT_OK;
 }
 
@@ -267,6 +340,24 @@ eat_status upload(eat_handle *h) {
 eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_out, cudaStream_t st) {
     uint32_t rounds = 0, sweeps = 0;
     eat_status e;
+    if (h->exchange == EAT_EXCHANGE_PEER) {
+        if (!h->peer_ready) return fail(EAT_ESTATE, "EAT_EXCHANGE_PEER: call eat_peer_connect on every rank first");
+        CUDA_TRY(eat::peer_query(h->d_peer_ix, h->peer_ctx, h->d_peer_ctx, h->d_peer_loc, h->d_perm, h->hx.n,
+                                 int(h->subwarp), s, t_s, d_out, st));
+        uint32_t w[2] = {0, 0};
+        CUDA_TRY(cudaMemcpyAsync(w, h->peer_loc[0].ctl + 8, 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        for (size_t g = 1; g < h->peer_loc.size(); ++g) {
+            uint32_t sg = 0;
+            CUDA_TRY(cudaMemcpy(&sg, h->peer_loc[g].ctl + 8, 4, cudaMemcpyDeviceToHost));
+            w[0] = std::max(w[0], sg);
+        }
+        h->st.last_rounds = w[1];
+        h->h_out1[h->hx.n] = w[0];
+        CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->h_out1 + h->hx.n, 4, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return EAT_OK;
+    }
     if (h->loopback) {
         std::vector<eat::DevIndex> ixs;
         std::vector<eat::PartWork *> ws;
@@ -422,7 +513,15 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     if (const char *dv = getenv("EAT_E2E_DIRECT")) h->e2e_direct = atoi(dv) != 0;  // A/B (tools/e2e_ab.py)
     h->part_rank = o.part_rank;
     h->part_count = pc;
-    h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 && !o.nccl_unique_id;
+    if (o.exchange > EAT_EXCHANGE_PEER) {
+        delete h;
+        return fail(EAT_EINVAL, "exchange must be EAT_EXCHANGE_ALLREDUCE or EAT_EXCHANGE_PEER");
+    }
+    h->exchange = o.exchange;
+    // all partitions in this process (one device) unless this is one rank of
+    // several processes (NCCL id given, or EAT_BUILD_MULTIPROCESS for PEER)
+    h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 &&
+                  (o.exchange == EAT_EXCHANGE_PEER ? !(o.flags & EAT_BUILD_MULTIPROCESS) : !o.nccl_unique_id);
     h->host_only = (o.flags & EAT_BUILD_HOST_ONLY) != 0;
     std::string msg;
     int rc = EAT_OK;
@@ -503,7 +602,7 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
                 break;
             }
         }
-        if (h->mode == EAT_MODE_EDGE_PARTITIONED && !h->loopback) {
+        if (h->mode == EAT_MODE_EDGE_PARTITIONED && !h->loopback && h->exchange == EAT_EXCHANGE_ALLREDUCE) {
             if (pc > 1) {
                 ncclUniqueId id;
                 std::memcpy(&id, o.nccl_unique_id, sizeof(id));
@@ -875,6 +974,47 @@ eat_status eat_index_export(const eat_handle *h, uint32_t *perm, uint32_t *type_
     if (type_rec) std::copy(x.type_rec.begin(), x.type_rec.end(), type_rec);
     if (crec) std::copy(x.crec.begin(), x.crec.end(), crec);
     if (pool) std::copy(x.pool.begin(), x.pool.end(), pool);
+    return EAT_OK;
+}
+
+eat_status eat_peer_export(eat_handle *h, void *handle_out) {
+    if (!h || !handle_out) return fail(EAT_EINVAL, "NULL argument");
+    if (h->mode != EAT_MODE_EDGE_PARTITIONED || h->exchange != EAT_EXCHANGE_PEER || h->loopback || h->peer_own.empty())
+        return fail(EAT_ESTATE, "eat_peer_export needs a multi-process EAT_EXCHANGE_PEER handle");
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_TRY(cudaSetDevice(h->device));
+    cudaIpcMemHandle_t ipc;
+    CUDA_TRY(cudaIpcGetMemHandle(&ipc, h->peer_own[0]));
+    static_assert(sizeof(ipc) == EAT_PEER_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle_out, &ipc, sizeof(ipc));
+    return EAT_OK;
+}
+
+eat_status eat_peer_connect(eat_handle *h, const void *handles, uint32_t count) {
+    if (!h || !handles) return fail(EAT_EINVAL, "NULL argument");
+    if (h->mode != EAT_MODE_EDGE_PARTITIONED || h->exchange != EAT_EXCHANGE_PEER || h->loopback)
+        return fail(EAT_ESTATE, "eat_peer_connect needs a multi-process EAT_EXCHANGE_PEER handle");
+    if (count != h->part_count) return fail(EAT_EINVAL, "eat_peer_connect: count must equal part_count");
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (h->peer_ready) return fail(EAT_ESTATE, "eat_peer_connect: already connected");
+    CUDA_TRY(cudaSetDevice(h->device));
+    const uint32_t n = h->hx.n;
+    eat::PeerCtx &c = h->peer_ctx;
+    for (uint32_t p = 0; p < count; ++p) {
+        if (p == h->part_rank) continue;
+        cudaIpcMemHandle_t ipc;
+        std::memcpy(&ipc, static_cast<const char *>(handles) + size_t(p) * EAT_PEER_HANDLE_BYTES, sizeof(ipc));
+        void *ptr = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&ptr, ipc, cudaIpcMemLazyEnablePeerAccess));
+        h->peer_mapped.push_back(ptr);
+        uint32_t lo = 0, hi = 0;
+        eat::partition_range(h->hx, p, count, lo, hi);
+        c.part[p] = eat::peer_part_view(ptr, n, lo, hi);
+        if (p == 0) c.gctl = eat::peer_gctl(ptr, n, hi - lo);
+    }
+    eat_status e = peer_publish(h);
+    if (e != EAT_OK) return e;
+    h->peer_ready = true;
     return EAT_OK;
 }
 

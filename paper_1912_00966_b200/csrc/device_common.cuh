@@ -193,8 +193,12 @@ __device__ __forceinline__ void push_aggregated(uint32_t v, uint32_t *q, uint32_
 
 // Relax one connection type (Algorithm 3) whose source has
 // arrival eu, against a global e[] (atomicMin).  Returns
-// the target v when this call strictly lowered e[v], else kNone.
-__device__ __forceinline__ uint32_t relax_type_global(const DevIndex &ix, uint64_t t, uint32_t eu, uint32_t *arr) {
+// the target v when this call strictly lowered e[v], else kNone; *cand_out
+// (optional) receives the candidate arrival.  SYS: system-scope atomic (e[]
+// also updated by peer GPUs, peer.cu).
+template <bool SYS = false>
+__device__ __forceinline__ uint32_t relax_type_global(const DevIndex &ix, uint64_t t, uint32_t eu, uint32_t *arr,
+                                                      uint32_t *cand_out = nullptr) {
     CrecPrefetch pf{};
     if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);
     const TypeRec tr = load_type(ix, t);
@@ -208,7 +212,8 @@ __device__ __forceinline__ uint32_t relax_type_global(const DevIndex &ix, uint64
     if (tc == kInf) return kNone;
     const uint32_t cand = tc + tr.lam;
     if (cand >= av) return kNone;
-    const uint32_t old = atomicMin(arr + tr.v, cand);
+    if (cand_out) *cand_out = cand;
+    const uint32_t old = SYS ? atomicMin_system(arr + tr.v, cand) : atomicMin(arr + tr.v, cand);
     return cand < old ? tr.v : kNone;
 }
 

@@ -48,7 +48,8 @@ class Engine:
                  host_only: bool = False, counters: bool = False, mode: str = "replicated", part_rank: int = 0, part_count: int = 1,
                  nccl_unique_id: Optional[bytes] = None, window: int = 0,
                  cta_threads: int = 0, subtrips: int = 0, trip=None, arr_bits: int = 0,
-                 cluster_dir: str = "auto", lookup: str = "cluster_ap", continuation: Optional[int] = None):
+                 cluster_dir: str = "auto", lookup: str = "cluster_ap", continuation: Optional[int] = None,
+                 exchange: str = "allreduce", multiprocess: bool = False):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
@@ -67,14 +68,16 @@ class Engine:
         opts = _lib.eat_build_opts(cluster_seconds=int(cluster_seconds), renumber=_lib.EAT_RENUMBER[renumber],
                                    device=int(device), kernel=_lib.EAT_KERNEL[kernel],
                                    flags=(_lib.EAT_BUILD_HOST_ONLY if host_only else 0)
-                                   | (_lib.EAT_BUILD_COUNTERS if counters else 0), subwarp=int(subwarp),
+                                   | (_lib.EAT_BUILD_COUNTERS if counters else 0)
+                                   | (_lib.EAT_BUILD_MULTIPROCESS if multiprocess else 0), subwarp=int(subwarp),
                                    mode=_lib.EAT_MODE[mode], part_rank=int(part_rank), part_count=int(part_count),
                                    nccl_unique_id=ctypes.cast(self._nccl_buf, ctypes.c_void_p) if self._nccl_buf else None,
                                    window_seconds=int(window), cta_threads=int(cta_threads),
                                    subtrips=int(subtrips), arr_bits=int(arr_bits),
                                    cluster_dir={"auto": 0, "dense": 1, "compact": 2}[cluster_dir],
                                    lookup={"cluster_ap": 0, "ap": 1, "linear": 2}[lookup],
-                                   continuation=0 if continuation is None else (int(continuation) or _lib.EAT_CONT_NONE))
+                                   continuation=0 if continuation is None else (int(continuation) or _lib.EAT_CONT_NONE),
+                                   exchange=_lib.EAT_EXCHANGE[exchange])
         self._h = _lib.eat_build(tt, opts)
         self.num_vertices = int(num_vertices)
         self.num_connections = int(m)
@@ -156,6 +159,14 @@ class Engine:
         _lib.eat_lookup_device(self._h, types.data_ptr(), bounds.data_ptr(), int(types.numel()), out.data_ptr(),
                                _stream_ptr(stream))
         return out
+
+    def peer_export(self) -> bytes:
+        """This rank's exchange-block handle (EAT_EXCHANGE_PEER, multiprocess)."""
+        return _lib.eat_peer_export(self._h)
+
+    def peer_connect(self, handles) -> None:
+        """Map every rank's block (handles in rank order; collective)."""
+        _lib.eat_peer_connect(self._h, handles)
 
     def partition_range(self, rank: int, count: int):
         """Internal-vertex range [lo, hi) owned by edge partition `rank` of `count`."""

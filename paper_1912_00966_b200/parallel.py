@@ -7,7 +7,11 @@ partitionings of the north star:
 * edge-partitioned single query (e2): every rank builds the index slice of
   its vertex range and libeat exchanges e[] with an NCCL min-allreduce per
   round; the NCCL unique id is created on rank 0 and broadcast over the
-  torch.distributed group (``edge_partitioned_engine``).
+  torch.distributed group (``edge_partitioned_engine``);
+* edge-partitioned with the in-kernel exchange (NEXT-2): the ranks' exchange
+  blocks are mapped into each other's address space with CUDA IPC handles
+  all-gathered over the torch.distributed group, and the query kernel lowers
+  remote vertices with peer atomics (``peer_partitioned_engine``).
 """
 from __future__ import annotations
 
@@ -94,3 +98,29 @@ def edge_partitioned_engine(tt, group=None, **kw):
     uid = nccl_unique_id(group) if world > 1 else None
     return Engine.from_timetable(tt, mode="edge_partitioned", part_rank=rank, part_count=world,
                                  nccl_unique_id=uid, **kw)
+
+
+def exchange_peer_handles(mine: bytes, group=None) -> list:
+    """All-gather every rank's exchange-block handle, in rank order."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = [None] * world
+    dist.all_gather_object(out, bytes(mine), group=group)
+    return [bytes(x) for x in out]
+
+
+def peer_partitioned_engine(tt, group=None, **kw):
+    """Collective: every rank builds the slice it owns with the peer exchange
+    (EAT_EXCHANGE_PEER), exports its block handle, all-gathers the handles
+    and maps the other ranks' blocks.  Queries are collective afterwards."""
+    import torch.distributed as dist
+
+    from .engine import Engine
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=rank, part_count=world, exchange="peer",
+                                multiprocess=True, **kw)
+    if world > 1:
+        eng.peer_connect(exchange_peer_handles(eng.peer_export(), group))
+    return eng

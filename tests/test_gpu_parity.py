@@ -246,6 +246,55 @@ def test_edge_partitioned_loopback(P):
         _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"loopback P={P} seed {seed}")
 
 
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8, 16])
+def test_edge_partitioned_peer_exchange_loopback(P):
+    """NEXT-2 on one GPU: P edge partitions as P CTA groups of one launch, the
+    exchange in-kernel (peer atomicMin on the owner's e[] + owner inbox +
+    cross-partition barrier in device memory) -- the code path a multi-GPU
+    run takes with IPC-mapped peer pointers."""
+    for name in ("tiny", "city"):
+        tt = synth.generate(name)
+        eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=P, exchange="peer",
+                                    subtrips=2 if name == "city" else 0)
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        rng = np.random.default_rng(100 + P)
+        qs = [synth.SINGLE_QUERY] + [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 86400))) for _ in range(6)]
+        for s, t_s in qs:  # repeated queries on one handle: round base / message slots carry over
+            _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"peer P={P} {name} ({s},{t_s})")
+            st = eng.stats()
+            assert st["last_rounds"] >= 1 and st["last_sweeps"] >= 1
+        eng.close()
+    for seed in range(60):
+        tt = synth.random_small(5000 + seed)
+        eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=P, exchange="peer",
+                                    subwarp=[32, 8, 1, 4][seed % 4], continuation=[None, 0, 3][seed % 3])
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        for k in range(2):
+            s, t_s = (seed + k) % tt.num_vertices, (seed * 7919 + k * 3001) % (2 * 86400)
+            _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"peer P={P} seed {seed}")
+        eng.close()
+
+
+def test_peer_exchange_api_errors():
+    tt = synth.generate("tiny")
+    loop = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=2, exchange="peer")
+    with pytest.raises(EatError) as e:
+        loop.peer_export()
+    assert e.value.status == _lib.EAT_ESTATE
+    rank1 = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=1, part_count=2, exchange="peer",
+                                  multiprocess=True)
+    assert len(rank1.peer_export()) == _lib.EAT_PEER_HANDLE_BYTES
+    with pytest.raises(EatError) as e:  # not connected yet
+        rank1.query(*synth.SINGLE_QUERY)
+    assert e.value.status == _lib.EAT_ESTATE
+    with pytest.raises(EatError) as e:
+        rank1.peer_connect([b"\0" * 64] * 3)
+    assert e.value.status == _lib.EAT_EINVAL
+    with pytest.raises(EatError) as e:
+        Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=17, exchange="peer")
+    assert e.value.status == _lib.EAT_EINVAL
+
+
 def test_edge_partitioned_single_rank():
     tt = synth.generate("tiny")
     eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=1)

@@ -126,9 +126,81 @@ def _edge_protocol(rank, world):
     return bool(ok)
 
 
+def _peer_handles(rank, world):
+    from paper_1912_00966_b200.parallel import exchange_peer_handles
+
+    got = exchange_peer_handles(bytes([rank + 1]) * 64)
+    return got == [bytes([r + 1]) * 64 for r in range(world)]
+
+
+def test_peer_handle_exchange_gloo():
+    """NEXT-2 plumbing: every rank gets all exchange-block handles in rank order."""
+    assert _run(_peer_handles) == {0: True, 1: True}
+
+
 def test_query_sharding_gloo():
     assert _run(_sharded_batch) == {0: True, 1: True}
 
 
 def test_edge_partition_protocol_gloo():
     assert _run(_edge_protocol) == {0: True, 1: True}
+
+
+def test_peer_exchange_protocol_model():
+    """NEXT-2 round protocol (peer.cu), modelled on the raw connections with a
+    random relaxation order: each partition drains its inbox, relaxes owned
+    vertices to local quiescence, lowers a remote vertex in its replica and in
+    the owner's e[] and, if the owner's value dropped, queues it once per round
+    in the owner's inbox; the query ends after a round with no message.  The
+    result must be the oracle's for every partition count and order."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import oracle
+    import synth
+    from paper_1912_00966_b200 import Engine
+
+    for seed in range(30):
+        tt = synth.random_small(7000 + seed)
+        n = tt.num_vertices
+        eng = Engine.from_timetable(tt, host_only=True)
+        perm = eng.export()["perm"].astype(np.int64)
+        rng = np.random.default_rng(seed)
+        for P in (1, 2, 3, 5):
+            rngs = [eng.partition_range(p, P) for p in range(P)]
+            owner = np.empty(n, np.int64)
+            for p, (lo, hi) in enumerate(rngs):
+                owner[(perm >= lo) & (perm < hi)] = p
+            out = {}
+            for i in range(tt.u.size):
+                out.setdefault(int(tt.u[i]), []).append((int(tt.v[i]), int(tt.dep[i]), int(tt.dur[i])))
+            s, t_s = int(rng.integers(n)), int(rng.integers(0, 2 * 86400))
+            arr = [np.full(n, INF, np.int64) for _ in range(P)]  # replicas
+            arr[owner[s]][s] = t_s
+            inbox = [set() for _ in range(P)]
+            frontier = [{s} if owner[s] == p else set() for p in range(P)]
+            rounds = 0
+            while True:
+                rounds += 1
+                new_inbox = [set() for _ in range(P)]
+                for p in rng.permutation(P):
+                    work = frontier[p] | inbox[p]
+                    while work:
+                        x = int(rng.choice(sorted(work)))
+                        work.discard(x)
+                        for (v, d, lam) in out.get(x, []):
+                            if arr[p][x] <= d and d + lam < arr[p][v]:
+                                arr[p][v] = d + lam
+                                o = owner[v]
+                                if o == p:
+                                    work.add(v)
+                                elif d + lam < arr[o][v]:
+                                    arr[o][v] = d + lam
+                                    new_inbox[o].add(v)
+                    frontier[p] = set()
+                inbox = new_inbox
+                if not any(inbox):
+                    break
+                assert rounds < 4 * n + 8
+            got = np.array([arr[owner[v]][v] for v in range(n)], np.uint32)
+            assert np.array_equal(got, oracle.csa(n, *tt.arrays(), s, t_s)), (seed, P)
