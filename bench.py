@@ -227,10 +227,21 @@ def run_single(args):
     tt = synth.generate(cfg)
     gen_s = time.perf_counter() - t0
     kw = dict(kw, subtrips=args.subtrips)
-    if kw.get("mode") == "edge_partitioned":
-        kw.update(part_rank=rank, part_count=world, nccl_unique_id=nccl_unique_id() if world > 1 else None)
+    mode_label = kw.get("mode", "replicated")
+    if mode_label == "edge_partitioned" and args.exchange == "peer":
+        desc = desc.replace("NCCL min-allreduce of e[] per exchange round",
+                            "in-kernel peer exchange: atomicMin on the owner's e[] over NVLink + inbox, NEXT-2")
     t0 = time.perf_counter()
-    eng = Engine.from_timetable(tt, device=dev, **kw)
+    if kw.get("mode") == "edge_partitioned" and args.exchange == "peer":
+        from paper_1912_00966_b200.parallel import peer_partitioned_engine
+
+        kw.pop("mode")
+        eng = peer_partitioned_engine(tt, device=dev, **kw) if world > 1 else Engine.from_timetable(
+            tt, device=dev, mode="edge_partitioned", exchange="peer", **kw)
+    else:
+        if kw.get("mode") == "edge_partitioned":
+            kw.update(part_rank=rank, part_count=world, nccl_unique_id=nccl_unique_id() if world > 1 else None)
+        eng = Engine.from_timetable(tt, device=dev, **kw)
     build_s = time.perf_counter() - t0
     st0 = eng.stats()
     s, t_s = synth.SINGLE_QUERY
@@ -289,7 +300,8 @@ def run_single(args):
                 "data": "synthetic",
                 "config": {"workload": f"{args.workload} ({desc})", "stops": tt.num_vertices,
                            "connections": tt.num_connections, "edges": st0["num_edges"], "types": st0["num_types"],
-                           "kernel": st0["kernel_name"], "mode": kw.get("mode", "replicated"),
+                           "kernel": st0["kernel_name"], "mode": mode_label,
+                           "exchange": args.exchange if mode_label == "edge_partitioned" else None,
                            "l2": "flushed (256 MiB write) between timed steps", "index_bytes": st0["index_bytes"],
                            "generate_s": gen_s, "build_s": build_s, "subtrips": args.subtrips,
                            "shortcuts": st0["num_shortcuts"]},
@@ -484,6 +496,9 @@ def main():
     ap.add_argument("--subtrips", type=int, default=2,
                     help="sub-trip shortcut scheme (PAPER.md:342-354): 0 off, 1 sqrt(k) per trip, 2 sqrt(avg)")
     ap.add_argument("--workload", default="city_batch", choices=["city_batch"] + sorted(SINGLE_WORKLOADS))
+    ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "peer"],
+                    help="country_part: per-round NCCL min-allreduce of e[] (BASELINE configs[4]) or the in-kernel "
+                         "peer exchange over NVLink (NEXT-2, CUDA IPC between the ranks)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

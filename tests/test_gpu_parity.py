@@ -419,3 +419,24 @@ def test_subtrips_parity(scheme):
             assert eng.stats()["num_shortcuts"] > 0
             _assert_rows(eng.query(*synth.SINGLE_QUERY), csa.query(*synth.SINGLE_QUERY), f"subtrips {name} {kernel}")
         _assert_rows(eng.query_many(src, ts), csa.query_many(src, ts), f"subtrips {name} batch")
+
+
+def test_peer_exchange_two_processes():
+    """EAT_EXCHANGE_PEER across processes: two torchrun ranks (sharing the
+    GPU when there is only one) map each other's exchange blocks with CUDA
+    IPC handles exchanged over torch.distributed and run collective queries
+    through system-scope peer atomics; every rank must return the oracle's e[]."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = 29000 + os.getpid() % 2000
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(root, "tests", "peer_mp_worker.py"), "tiny"]
+    env = dict(os.environ, EAT_GRID_CTAS_PER_SM="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env=env, cwd=root)
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert sorted(d["rank"] for d in lines) == [0, 1] and all(d["parity"] for d in lines), lines
