@@ -30,15 +30,25 @@ using namespace dev;
 }  // namespace
 
 // CTAs per SM of the persistent grid kernels (fewer CTAs = cheaper grid
-// barrier): EAT_GRID_CTAS_PER_SM (1..8, default 4; tuning knob).
+// barrier): EAT_GRID_CTAS_PER_SM (1..8, default 1 -- the kernels use
+// 1024-thread CTAs; tuning knob).
 int grid_ctas_per_sm() {
     static int v = [] {
         const char *e = getenv("EAT_GRID_CTAS_PER_SM");
-        int x = e ? atoi(e) : 4;
+        int x = e ? atoi(e) : 1;
         return x < 1 ? 1 : (x > 8 ? 8 : x);
     }();
     return v;
 }
+
+#ifdef EAT_EXP_TRACE
+__device__ unsigned long long g_trace[4096 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 namespace {
 
@@ -421,10 +431,13 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
 // SCHED == kSchedFull: topology-driven full sweep, one thread per connection
 // type, active test on a bitmap (the paper's thread-per-type schedule,
 // PAPER.md:228, 305).
-constexpr int kGridThreads = 256;
+// 1024-thread CTAs, one per SM: the same 32 warps per SM as 4 x 256 with a
+// quarter of the grid-barrier arrivals (metro -10 %, country -9 %;
+// DESIGN.md §9).
+constexpr int kGridThreads = 1024;
 
 template <int SW, int SCHED>
-__global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWork w, uint32_t s, uint32_t ts,
+__global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, GridWork w, uint32_t s, uint32_t ts,
                                                              uint32_t *out) {
     const uint32_t n = ix.n;
     const uint32_t W = (n + 31u) / 32u;
@@ -460,6 +473,12 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
     for (;;) {
         const uint32_t c_cur = sweep % 3u, c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
         if (gtid == 0) w.ctl[c_old] = 0;
+#ifdef EAT_EXP_TRACE
+        if (gtid == 0 && sweep < 4096) {
+            g_trace[sweep * 4 + 0] = gtimer();
+            g_trace[sweep * 4 + 3] = ld_cg(w.ctl + c_cur);
+        }
+#endif
         if (SCHED == kSchedFlat) {
             // worklist + time window + warp-flattened (vertex, type) pairs
             const uint32_t cnt = ld_cg(w.ctl + c_cur);
@@ -617,7 +636,14 @@ __global__ void __launch_bounds__(kGridThreads) k_query_grid(DevIndex ix, GridWo
             }
             if (__any_sync(0xFFFFFFFFu, improved) && (threadIdx.x & 31u) == 0) atomicExch(w.ctl + c_nxt, 1u);
         }
+#ifdef EAT_EXP_TRACE
+        __syncthreads();
+        if (threadIdx.x == 0 && sweep < 4096) atomicMax(&g_trace[sweep * 4 + 1], gtimer());
+#endif
         grid_sync(bar);
+#ifdef EAT_EXP_TRACE
+        if (gtid == 0 && sweep < 4096) g_trace[sweep * 4 + 2] = gtimer();
+#endif
         ++sweep;
         if (ld_cg(w.ctl + c_nxt) == 0u) break;
     }
@@ -776,3 +802,14 @@ cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const 
 }
 
 }  // namespace eat
+
+#ifdef EAT_EXP_TRACE
+extern "C" int eat_debug_trace(unsigned long long *out, int clear) {
+    if (cudaMemcpyFromSymbol(out, eat::g_trace, sizeof(eat::g_trace)) != cudaSuccess) return 1;
+    if (clear) {
+        static unsigned long long z[4096 * 4];
+        cudaMemcpyToSymbol(eat::g_trace, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

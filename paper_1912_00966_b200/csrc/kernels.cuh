@@ -70,7 +70,7 @@ cudaError_t launch_query_cta(const DevIndex &ix, const CtaArgs &a, cudaStream_t 
 cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,
                               uint32_t t_s, uint32_t *d_out, cudaStream_t st);
 
-// CTAs per SM of the persistent grid kernels (env EAT_GRID_CTAS_PER_SM, default 4).
+// CTAs per SM of the persistent grid kernels (env EAT_GRID_CTAS_PER_SM, default 1).
 int grid_ctas_per_sm();
 
 // Occupancy-derived grid size of the CTA kernel variant for n vertices (0 if e[] does not fit).

@@ -23,7 +23,7 @@ namespace {
 
 using namespace dev;
 
-constexpr int kPartThreads = 256;
+constexpr int kPartThreads = 1024;  // one CTA per SM, as the grid kernels
 
 template <int SW>
 __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWork w, uint32_t lo, uint32_t hi,

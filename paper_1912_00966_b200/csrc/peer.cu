@@ -30,7 +30,7 @@ namespace {
 
 using namespace dev;
 
-constexpr int kPeerThreads = 256;
+constexpr int kPeerThreads = 1024;  // one CTA per SM per group, as the grid kernels
 
 __device__ __forceinline__ uint32_t ld_sys(uint32_t *p) {
     return cuda::atomic_ref<uint32_t, cuda::thread_scope_system>(*p).load(cuda::memory_order_relaxed);
