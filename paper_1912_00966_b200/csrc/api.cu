@@ -342,8 +342,8 @@ eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_
     eat_status e;
     if (h->exchange == EAT_EXCHANGE_PEER) {
         if (!h->peer_ready) return fail(EAT_ESTATE, "EAT_EXCHANGE_PEER: call eat_peer_connect on every rank first");
-        CUDA_TRY(eat::peer_query(h->d_peer_ix, h->peer_ctx, h->d_peer_ctx, h->d_peer_loc, h->d_perm, h->hx.n,
-                                 int(h->subwarp), s, t_s, d_out, st));
+        CUDA_TRY(eat::peer_query(h->d_peer_ix, h->peer_ctx, h->d_peer_ctx, h->peer_loc.data(), h->d_peer_loc, h->d_perm,
+                                 h->hx.n, int(h->subwarp), s, t_s, d_out, st));
         uint32_t w[2] = {0, 0};
         CUDA_TRY(cudaMemcpyAsync(w, h->peer_loc[0].ctl + 8, 8, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));

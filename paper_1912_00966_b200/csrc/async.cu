@@ -47,7 +47,8 @@ __global__ void __launch_bounds__(kAsyncThreads, 1) k_query_async(DevIndex ix, A
     __shared__ uint32_t s_cnt[2], s_more[2];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
     const uint64_t gtid = uint64_t(c) * kAsyncThreads + tid, gsz = uint64_t(P) * kAsyncThreads;
-    uint32_t *bar = w.ctl + 4;
+    uint32_t *bar = w.ctl + 4;  // monotonic barrier counter (zeroed per launch)
+    uint32_t bar_epoch = 0;
 
     // ---- init (Algorithm 2)
     for (uint64_t i = gtid; i < n; i += gsz) {
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 1) k_query_async(DevIndex ix, A
     for (uint32_t i = tid; i < span; i += kAsyncThreads) sarr[i] = kInf;
     for (uint32_t i = tid; i < Wl; i += kAsyncThreads) bmD[i] = bmN[i] = 0;
     if (tid == 0) s_cnt[0] = s_cnt[1] = s_more[0] = s_more[1] = 0;
-    grid_sync(bar);
+    grid_sync(bar, bar_epoch);
     const uint32_t si = __ldg(ix.perm + s);
     if (tid == 0 && si >= lo && si < hi) {
         sarr[si - lo] = ts;
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 1) k_query_async(DevIndex ix, A
         nmsg = __reduce_add_sync(0xFFFFFFFFu, nmsg);
         if (lane == 0 && nmsg) atomicAdd(w.ctl + r % 3u, nmsg);
         // ---- 3. exchange barrier
-        grid_sync(bar);
+        grid_sync(bar, bar_epoch);
         if (ld_cg(w.ctl + r % 3u) == 0u) {
             if (tid == 0) {
                 atomicMax(w.ctl + 9, total_sweeps);
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 1) k_query_async(DevIndex ix, A
             break;
         }
     }
-    grid_sync(bar);
+    grid_sync(bar, bar_epoch);
     for (uint64_t i = gtid; i < n; i += gsz) out[i] = ld_cg(w.garr + __ldg(ix.perm + i));
 }
 

@@ -443,7 +443,8 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
     const uint32_t W = (n + 31u) / 32u;
     const uint64_t gtid = blockIdx.x * uint64_t(kGridThreads) + threadIdx.x;
     const uint64_t gsz = uint64_t(gridDim.x) * kGridThreads;
-    uint32_t *bar = w.ctl + 4;
+    uint32_t *bar = w.ctl + 4;  // monotonic barrier counter (zeroed per launch)
+    uint32_t bar_epoch = 0;
     // Initialize (Algorithm 2)
     for (uint64_t i = gtid; i < n; i += gsz) {
         w.arr[i] = kInf;
@@ -460,14 +461,14 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
         w.ctl[12] = kInf;
         w.ctl[13] = kInf;
     }
-    grid_sync(bar);
+    grid_sync(bar, bar_epoch);
     if (gtid == 0) {
         const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
         w.arr[si] = ts;
         if (!kBitmapSched) w.q0[0] = si;
         else w.bm[si >> 5] = 1u << (si & 31u);
     }
-    grid_sync(bar);
+    grid_sync(bar, bar_epoch);
 
     uint32_t sweep = 0;
     for (;;) {
@@ -640,7 +641,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
         __syncthreads();
         if (threadIdx.x == 0 && sweep < 4096) atomicMax(&g_trace[sweep * 4 + 1], gtimer());
 #endif
-        grid_sync(bar);
+        grid_sync(bar, bar_epoch);
 #ifdef EAT_EXP_TRACE
         if (gtid == 0 && sweep < 4096) g_trace[sweep * 4 + 2] = gtimer();
 #endif

@@ -33,7 +33,7 @@ struct GridWork {
     uint32_t *q0, *q1;   // [n] frontier worklists (ping-pong)
     uint32_t *stamp;     // [n] "queued for sweep k" stamps (dedup)
     uint32_t *bm;        // [3*W] rotating active bitmaps (full-sweep schedule)
-    uint32_t *ctl;       // [16] control words: 0-2 rotating counters, 4-5 grid barrier, 8 sweeps, 11-13 window base
+    uint32_t *ctl;       // [16] control words: 0-2 rotating counters, 4 grid barrier counter, 8 sweeps, 11-13 window base
 };
 
 enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2, kSchedConn = 3, kSchedBitmap = 4 };

@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
     const uint32_t n = ix.n;
     const uint64_t gtid = blockIdx.x * uint64_t(kPartThreads) + threadIdx.x;
     const uint64_t gsz = uint64_t(gridDim.x) * kPartThreads;
-    uint32_t *bar = w.ctl + 4;
+    uint32_t *bar = w.ctl + 4;  // monotonic barrier counter (zeroed per launch)
+    uint32_t bar_epoch = 0;
     if (first) {
         for (uint64_t i = gtid; i < n; i += gsz) {
             w.arr[i] = kInf;
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
             w.stamp[i] = 0;
         }
         if (gtid == 0) w.ctl[8] = 0, w.ctl[10] = 0;
-        grid_sync(bar);
+        grid_sync(bar, bar_epoch);
         if (gtid == 0) w.arr[__ldg(ix.perm + s)] = ts;  // caller id -> internal id
     }
     if (gtid == 0) {
@@ -48,11 +49,11 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
         w.ctl[1] = 0;
         w.ctl[2] = 0;
     }
-    grid_sync(bar);
+    grid_sync(bar, bar_epoch);
     // initial local frontier: owned vertices lowered since the last exchange
     for (uint64_t v = lo + gtid; v < hi; v += gsz)
         if (ld_cg(w.arr + v) < ld_cg(w.prev + v)) push_aggregated(uint32_t(v), w.q0, w.ctl + 0);
-    grid_sync(bar);
+    grid_sync(bar, bar_epoch);
     const uint32_t base = ld_cg(w.ctl + 10);
     bool remote = false;
     uint32_t sweep = 0;
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
                 --budget;
             }
         }
-        grid_sync(bar);
+        grid_sync(bar, bar_epoch);
         ++sweep;
         if (ld_cg(w.ctl + c_nxt) == 0u) break;
         if (w.local_sweeps_per_round && sweep >= w.local_sweeps_per_round) {
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
         }
     }
     if (__any_sync(0xFFFFFFFFu, remote) && (threadIdx.x & 31u) == 0) atomicExch(w.arr + n, 0u);
-    grid_sync(bar);
+    grid_sync(bar, bar_epoch);
     // prev := what this rank contributes to the exchange; vertices left on a
     // bounded local frontier (stamp == ~0) keep prev = INF so they re-enter.
     for (uint64_t i = gtid; i < n; i += gsz) {

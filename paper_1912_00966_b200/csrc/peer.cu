@@ -36,32 +36,13 @@ __device__ __forceinline__ uint32_t ld_sys(uint32_t *p) {
     return cuda::atomic_ref<uint32_t, cuda::thread_scope_system>(*p).load(cuda::memory_order_relaxed);
 }
 
-// Barrier of the nctas CTAs of one group (counter pair in the group's own memory).
-__device__ __forceinline__ void group_sync(uint32_t *bar, uint32_t nctas) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cnt(bar[0]);
-        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> gen(bar[1]);
-        const uint32_t g = gen.load(cuda::memory_order_relaxed);
-        __threadfence();
-        if (cnt.fetch_add(1u, cuda::memory_order_acq_rel) == nctas - 1u) {
-            cnt.store(0u, cuda::memory_order_relaxed);
-            gen.fetch_add(1u, cuda::memory_order_release);
-        } else {
-            while (gen.load(cuda::memory_order_acquire) == g) {
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
 // Barrier of all partitions (every group of every launch, possibly on other
 // GPUs): the group meets, then its leader meets the other leaders on the
 // system-scope counter pair in partition 0's block, then the group meets again.
-__device__ __forceinline__ void peer_sync(uint32_t *lbar, uint32_t nctas, uint32_t *gctl, uint32_t P, bool leader) {
+__device__ __forceinline__ void peer_sync(uint32_t *lbar, uint32_t &lep, uint32_t nctas, uint32_t *gctl, uint32_t P,
+                                          bool leader) {
     __threadfence_system();  // this thread's peer writes before anyone leaves the barrier
-    group_sync(lbar, nctas);
+    grid_sync(lbar, lep, nctas);
     if (leader && threadIdx.x == 0) {
         cuda::atomic_ref<uint32_t, cuda::thread_scope_system> cnt(gctl[0]);
         cuda::atomic_ref<uint32_t, cuda::thread_scope_system> gen(gctl[1]);
@@ -76,7 +57,7 @@ __device__ __forceinline__ void peer_sync(uint32_t *lbar, uint32_t nctas, uint32
         }
         __threadfence_system();
     }
-    group_sync(lbar, nctas);
+    grid_sync(lbar, lep, nctas);
 }
 
 __device__ __forceinline__ uint32_t owner_of(const PeerCtx &ctx, uint32_t v) {
@@ -98,7 +79,8 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
     const PeerPart me = ctx.part[p];
     const uint32_t n = ix.n, lo = me.lo, hi = me.hi, own = hi - lo;
     const uint64_t gtid = uint64_t(crank) * kPeerThreads + threadIdx.x, gsz = uint64_t(cpg) * kPeerThreads;
-    uint32_t *lbar = loc.ctl + 4;
+    uint32_t *lbar = loc.ctl + 4;  // the group's monotonic barrier counter (zeroed per launch)
+    uint32_t lep = 0;
     const bool leader = crank == 0;
     const uint32_t rbase = ld_cg(loc.ctl + 10);  // absolute round of this query's round 0 (slots, parity)
 
@@ -112,7 +94,7 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
         loc.ctl[0] = loc.ctl[1] = loc.ctl[2] = 0;
         me.inbox_cnt[0] = me.inbox_cnt[1] = 0;
     }
-    peer_sync(lbar, cpg, ctx.gctl, ctx.P, leader);  // nobody relaxes into a replica before it is initialized
+    peer_sync(lbar, lep, cpg, ctx.gctl, ctx.P, leader);  // nobody relaxes into a replica before it is initialized
     if (gtid == 0) {
         const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
         if (si >= lo && si < hi) {
@@ -121,7 +103,7 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
             loc.ctl[0] = 1;
         }
     }
-    group_sync(lbar, cpg);
+    grid_sync(lbar, lep, cpg);
 
     const uint32_t lane = uint32_t(gtid % SW);
     const uint32_t wl = threadIdx.x & 31u;
@@ -143,7 +125,7 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
         if (p == 0 && leader && threadIdx.x == 0)  // message slot of the next round (read two barriers ago)
             cuda::atomic_ref<uint32_t, cuda::thread_scope_system>(ctx.gctl[2 + (ra + 1u) % 3u])
                 .store(0u, cuda::memory_order_relaxed);
-        group_sync(lbar, cpg);
+        grid_sync(lbar, lep, cpg);
         if (r > 0 && gtid == 0) me.inbox_cnt[pin ^ 1u] = 0;  // refilled only in round r+1
 
         // ---- 2. local sweeps to quiescence
@@ -192,7 +174,7 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
                     --budget;
                 }
             }
-            group_sync(lbar, cpg);
+            grid_sync(lbar, lep, cpg);
             ++sweep;
             if (ld_cg(loc.ctl + c_nxt) == 0u) break;
         }
@@ -200,7 +182,7 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
         // ---- 3. exchange barrier; stop after a round without messages
         nmsg = __reduce_add_sync(0xFFFFFFFFu, nmsg);
         if (wl == 0 && nmsg) atomicAdd_system(ctx.gctl + 2 + ra % 3u, nmsg);
-        peer_sync(lbar, cpg, ctx.gctl, ctx.P, leader);
+        peer_sync(lbar, lep, cpg, ctx.gctl, ctx.P, leader);
         if (ld_sys(ctx.gctl + 2 + ra % 3u) == 0u) break;
     }
     if (gtid == 0) {
@@ -269,10 +251,12 @@ void peer_local_free(PeerLocal &l) {
     l = PeerLocal{};
 }
 
-cudaError_t peer_query(const DevIndex *d_ix, const PeerCtx &ctx, const PeerCtx *d_ctx, PeerLocal *d_loc,
-                       const uint32_t *d_perm, uint32_t n, int subwarp, uint32_t s, uint32_t t_s, uint32_t *d_out,
-                       cudaStream_t st) {
+cudaError_t peer_query(const DevIndex *d_ix, const PeerCtx &ctx, const PeerCtx *d_ctx, const PeerLocal *h_loc,
+                       PeerLocal *d_loc, const uint32_t *d_perm, uint32_t n, int subwarp, uint32_t s, uint32_t t_s,
+                       uint32_t *d_out, cudaStream_t st) {
     cudaError_t e;
+    for (uint32_t g = 0; g < ctx.groups; ++g)  // group barrier counters restart at 0
+        if ((e = cudaMemsetAsync(h_loc[g].ctl + 4, 0, sizeof(uint32_t), st)) != cudaSuccess) return e;
     switch (subwarp) {
         case 1: e = launch_peer_sw<1>(d_ix, ctx, d_ctx, d_loc, s, t_s, st); break;
         case 2: e = launch_peer_sw<2>(d_ix, ctx, d_ctx, d_loc, s, t_s, st); break;

@@ -47,7 +47,7 @@ struct PeerCtx {
 // Per partition run by this launch (memory of the launching device).
 struct PeerLocal {
     uint32_t *q0, *q1, *stamp;  // [n] local frontier worklists + dedup stamps
-    uint32_t *ctl;              // [16]: 0-2 frontier counters, 4-5 group barrier, 8 sweeps, 9 rounds, 10 round base
+    uint32_t *ctl;              // [16]: 0-2 frontier counters, 4 group barrier counter, 8 sweeps, 9 rounds, 10 round base
 };
 
 // Bytes of one exchange block (offsets below are identical on every rank).
@@ -65,8 +65,8 @@ void peer_local_free(PeerLocal &l);
 // One query: a cooperative launch of ctx.groups CTA groups (d_ix[g] is group
 // g's index slice, d_ctx / d_loc device copies), then the caller-ordered
 // gather of the owners' e[] into d_out.  Collective across all partitions.
-cudaError_t peer_query(const DevIndex *d_ix, const PeerCtx &ctx, const PeerCtx *d_ctx, PeerLocal *d_loc,
-                       const uint32_t *d_perm, uint32_t n, int subwarp, uint32_t s, uint32_t t_s, uint32_t *d_out,
-                       cudaStream_t st);
+cudaError_t peer_query(const DevIndex *d_ix, const PeerCtx &ctx, const PeerCtx *d_ctx, const PeerLocal *h_loc,
+                       PeerLocal *d_loc, const uint32_t *d_perm, uint32_t n, int subwarp, uint32_t s, uint32_t t_s,
+                       uint32_t *d_out, cudaStream_t st);
 
 }  // namespace eat

@@ -27,6 +27,33 @@ __device__ __forceinline__ void grid_sync(unsigned *bar) {
     __syncthreads();
 }
 __global__ void k_bar(unsigned *bar, int iters) { for (int i = 0; i < iters; ++i) grid_sync(bar); }
+// monotonic-counter barrier: red.release arrive, acquire-poll the same word
+__device__ __forceinline__ void grid_sync_mono(unsigned *cnt, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(cnt) : "memory");
+        unsigned v;
+        do { asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory"); } while (v < target);
+    }
+    __syncthreads();
+}
+__global__ void k_bar_mono(unsigned *bar, int iters) {
+    for (int i = 0; i < iters; ++i) grid_sync_mono(bar, (unsigned)(i + 1) * gridDim.x);
+}
+// same without acquire/release on the poll (relaxed + fences)
+__device__ __forceinline__ void grid_sync_mono_f(unsigned *cnt, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(cnt, 1u);
+        while (*(volatile unsigned *)cnt < target) {}
+        __threadfence();
+    }
+    __syncthreads();
+}
+__global__ void k_bar_mono_f(unsigned *bar, int iters) {
+    for (int i = 0; i < iters; ++i) grid_sync_mono_f(bar, (unsigned)(i + 1) * gridDim.x);
+}
 __global__ void k_chase(const unsigned *next, int hops, unsigned *out) {
     unsigned x = 0;
     for (int i = 0; i < hops; ++i) x = __ldcg(next + x);
@@ -41,14 +68,16 @@ __global__ void k_atom(unsigned *a, int hops, unsigned *out, int kind) {
     }
     out[0] = x;
 }
-double bar_us(int grid, int iters) {
+double bar_us(int grid, int iters, int kind, int threads) {
     auto bar = torch::zeros({2}, torch::dtype(torch::kInt32).device(torch::kCUDA));
     unsigned *b = (unsigned *)bar.data_ptr();
     void *args[] = {&b, &iters};
+    void *k = kind == 0 ? (void *)k_bar : (kind == 1 ? (void *)k_bar_mono : (void *)k_bar_mono_f);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    cudaLaunchCooperativeKernel((void *)k_bar, dim3(grid), dim3(256), args, 0, 0);
+    cudaLaunchCooperativeKernel(k, dim3(grid), dim3(threads), args, 0, 0);
+    cudaMemset(b, 0, 8);
     cudaEventRecord(e0);
-    cudaLaunchCooperativeKernel((void *)k_bar, dim3(grid), dim3(256), args, 0, 0);
+    cudaLaunchCooperativeKernel(k, dim3(grid), dim3(threads), args, 0, 0);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     return ms * 1000.0 / iters;
@@ -74,12 +103,14 @@ double atom_ns(torch::Tensor a, int hops, int kind) {
     return ms * 1e6 / hops;
 }
 '''
-m = load_inline("latbench", cpp_sources="double bar_us(int, int); double chase_ns(torch::Tensor, int); double atom_ns(torch::Tensor, int, int);",
+m = load_inline("latbench", cpp_sources="double bar_us(int, int, int, int); double chase_ns(torch::Tensor, int); double atom_ns(torch::Tensor, int, int);",
                 cuda_sources=src, functions=["bar_us", "chase_ns", "atom_ns"],
                 extra_cuda_cflags=["-gencode", "arch=compute_100a,code=sm_100a", "-O3"], verbose=False)
 res = {}
 for g in (148, 296, 592, 1184):
-    res[f"grid_sync_us_{g}ctas"] = m.bar_us(g, 2000)
+    res[f"grid_sync_us_{g}ctas"] = m.bar_us(g, 2000, 0, 256)
+for kind, name in ((0, "gen"), (1, "mono_acqrel"), (2, "mono_fence")):
+    res[f"grid_sync_{name}_us_148x1024"] = m.bar_us(148, 2000, kind, 1024)
 for mb in (1, 64, 1024):
     n = mb * 1024 * 1024 // 4
     perm = torch.randperm(n, dtype=torch.int64)
