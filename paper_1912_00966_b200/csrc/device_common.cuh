@@ -165,7 +165,13 @@ __device__ __forceinline__ uint32_t type_lookup_ablation(const DevIndex &ix, con
 // counter reaches epoch * nctas -- one fire-and-forget atomic per CTA and a
 // poll, 1.3 us for 148 CTAs on B200 vs 2.5 us for a count/reset/generation
 // barrier (tools/latency_bench.py).  `epoch` is the caller's barrier count.
-__device__ __forceinline__ void grid_sync(uint32_t *cnt, uint32_t &epoch, uint32_t nctas) {
+// With `rd`, thread 0 also reads *rd after the barrier and every thread gets
+// that value: a control word all CTAs need (frontier size, stop flag) is
+// fetched once per CTA instead of by every warp -- thousands of same-line
+// reads right after the barrier cost ~1 us (tools/trace_sweeps.py).
+__device__ __forceinline__ uint32_t grid_sync(uint32_t *cnt, uint32_t &epoch, uint32_t nctas,
+                                              const uint32_t *rd = nullptr) {
+    __shared__ uint32_t s_bcast;
     __syncthreads();
     ++epoch;
     if (threadIdx.x == 0) {
@@ -175,11 +181,15 @@ __device__ __forceinline__ void grid_sync(uint32_t *cnt, uint32_t &epoch, uint32
         while (*reinterpret_cast<volatile uint32_t *>(cnt) < target) {
         }
         __threadfence();
+        if (rd) s_bcast = __ldcg(rd);
     }
     __syncthreads();
+    return rd ? s_bcast : 0u;
 }
 
-__device__ __forceinline__ void grid_sync(uint32_t *cnt, uint32_t &epoch) { grid_sync(cnt, epoch, gridDim.x); }
+__device__ __forceinline__ uint32_t grid_sync(uint32_t *cnt, uint32_t &epoch, const uint32_t *rd = nullptr) {
+    return grid_sync(cnt, epoch, gridDim.x, rd);
+}
 
 // Warp-aggregated append of v to a worklist (one global atomic per group of
 // converged pushing lanes).

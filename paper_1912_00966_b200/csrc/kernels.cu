@@ -43,9 +43,16 @@ int grid_ctas_per_sm() {
 
 #ifdef EAT_EXP_TRACE
 __device__ unsigned long long g_trace[4096 * 4];
+__device__ unsigned long long g_trace2[4096 * 8];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// timer read that waits for `dep` (scoreboard on the input register)
+__device__ __forceinline__ unsigned long long gtimer_dep(uint32_t dep) {
+    unsigned long long t;
+    asm volatile("{ .reg .u32 d; mov.u32 d, %1; mov.u64 %0, %%globaltimer; }" : "=l"(t) : "r"(dep));
     return t;
 }
 #endif
@@ -468,7 +475,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
         if (!kBitmapSched) w.q0[0] = si;
         else w.bm[si >> 5] = 1u << (si & 31u);
     }
-    grid_sync(bar, bar_epoch);
+    uint32_t cnt_cur = grid_sync(bar, bar_epoch, w.ctl + 0);  // sweep 0's frontier size (1)
 
     uint32_t sweep = 0;
     for (;;) {
@@ -482,7 +489,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
 #endif
         if (SCHED == kSchedFlat) {
             // worklist + time window + warp-flattened (vertex, type) pairs
-            const uint32_t cnt = ld_cg(w.ctl + c_cur);
+            const uint32_t cnt = cnt_cur;
             const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
             uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
             const uint32_t t_cur = sweep % 3u, t_nxt = (sweep + 1u) % 3u, t_old = (sweep + 2u) % 3u;
@@ -548,7 +555,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
                 }
             }
         } else if (SCHED == kSchedFrontier) {
-            const uint32_t cnt = ld_cg(w.ctl + c_cur);
+            const uint32_t cnt = cnt_cur;
             const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
             uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
             const uint32_t lane = uint32_t(gtid % SW);
@@ -561,11 +568,19 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
             const uint32_t wl = threadIdx.x & 31u;
             const unsigned smask = SW == 32 ? 0xFFFFFFFFu : (((1u << SW) - 1u) << (wl & ~(SW - 1u)));
             for (uint64_t it = gtid / SW; it < cnt; it += gsz / SW) {
+#ifdef EAT_EXP_TRACE
+                const bool tr0 = gtid == 0 && it == 0 && sweep < 4096;
+                uint32_t hop = 0;
+                if (tr0) g_trace2[sweep * 8 + 0] = gtimer();
+#endif
                 uint32_t x = ld_cg(qc + it);
                 uint32_t budget = ix.cont_budget;
                 for (;;) {
                     const uint32_t eu = ld_cg(w.arr + x);
                     const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
+#ifdef EAT_EXP_TRACE
+                    if (tr0 && hop < 2) g_trace2[sweep * 8 + 1 + hop * 3] = gtimer_dep(eu + p1);
+#endif
                     uint32_t cv = kNone;
                     for (uint32_t t = p0 + lane; t < p1; t += SW) {
                         const uint32_t v = relax_type_global(ix, t, eu, w.arr);
@@ -573,7 +588,14 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
                         if (budget > 0 && cv == kNone) cv = v;
                         else if (atomicExch(w.stamp + v, sweep + 1u) != sweep + 1u) push_aggregated(v, qn, w.ctl + c_nxt);
                     }
+#ifdef EAT_EXP_TRACE
+                    if (tr0 && hop < 2) g_trace2[sweep * 8 + 2 + hop * 3] = gtimer_dep(cv);
+#endif
                     const unsigned cm = __ballot_sync(smask, cv != kNone) & smask;
+#ifdef EAT_EXP_TRACE
+                    if (tr0 && hop < 2) g_trace2[sweep * 8 + 3 + hop * 3] = gtimer_dep(cm);
+                    ++hop;
+#endif
                     if (!cm) break;
                     const uint32_t src = __ffs(cm) - 1u;
                     const uint32_t nx = __shfl_sync(smask, cv, src);
@@ -641,12 +663,12 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
         __syncthreads();
         if (threadIdx.x == 0 && sweep < 4096) atomicMax(&g_trace[sweep * 4 + 1], gtimer());
 #endif
-        grid_sync(bar, bar_epoch);
+        cnt_cur = grid_sync(bar, bar_epoch, w.ctl + c_nxt);  // next frontier size / improved flag
 #ifdef EAT_EXP_TRACE
         if (gtid == 0 && sweep < 4096) g_trace[sweep * 4 + 2] = gtimer();
 #endif
         ++sweep;
-        if (ld_cg(w.ctl + c_nxt) == 0u) break;
+        if (cnt_cur == 0u) break;
     }
     for (uint64_t i = gtid; i < n; i += gsz) out[i] = ld_cg(w.arr + __ldg(ix.perm + i));
     if (gtid == 0) w.ctl[8] = sweep;
@@ -805,6 +827,9 @@ cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const 
 }  // namespace eat
 
 #ifdef EAT_EXP_TRACE
+extern "C" int eat_debug_trace2(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, eat::g_trace2, sizeof(eat::g_trace2)) != cudaSuccess;
+}
 extern "C" int eat_debug_trace(unsigned long long *out, int clear) {
     if (cudaMemcpyFromSymbol(out, eat::g_trace, sizeof(eat::g_trace)) != cudaSuccess) return 1;
     if (clear) {

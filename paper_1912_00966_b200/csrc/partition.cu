@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
     // initial local frontier: owned vertices lowered since the last exchange
     for (uint64_t v = lo + gtid; v < hi; v += gsz)
         if (ld_cg(w.arr + v) < ld_cg(w.prev + v)) push_aggregated(uint32_t(v), w.q0, w.ctl + 0);
-    grid_sync(bar, bar_epoch);
+    uint32_t cnt_cur = grid_sync(bar, bar_epoch, w.ctl + 0);  // sweep 0's frontier size
     const uint32_t base = ld_cg(w.ctl + 10);
     bool remote = false;
     uint32_t sweep = 0;
@@ -61,9 +61,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
     const uint32_t wl = threadIdx.x & 31u;
     const unsigned smask = SW == 32 ? 0xFFFFFFFFu : (((1u << SW) - 1u) << (wl & ~(SW - 1u)));
     for (;;) {
-        const uint32_t c_cur = sweep % 3u, c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
+        const uint32_t c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
         if (gtid == 0) w.ctl[c_old] = 0;
-        const uint32_t cnt = ld_cg(w.ctl + c_cur);
+        const uint32_t cnt = cnt_cur;
         const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
         uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
         const uint32_t stamp = base + sweep + 1u;
@@ -97,9 +97,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
                 --budget;
             }
         }
-        grid_sync(bar, bar_epoch);
+        cnt_cur = grid_sync(bar, bar_epoch, w.ctl + c_nxt);
         ++sweep;
-        if (ld_cg(w.ctl + c_nxt) == 0u) break;
+        if (cnt_cur == 0u) break;
         if (w.local_sweeps_per_round && sweep >= w.local_sweeps_per_round) {
             // bounded local phase: leftover frontier vertices stay "lowered since
             // the last exchange" only if prev is not refreshed for them, so

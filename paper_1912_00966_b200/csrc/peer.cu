@@ -125,15 +125,15 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
         if (p == 0 && leader && threadIdx.x == 0)  // message slot of the next round (read two barriers ago)
             cuda::atomic_ref<uint32_t, cuda::thread_scope_system>(ctx.gctl[2 + (ra + 1u) % 3u])
                 .store(0u, cuda::memory_order_relaxed);
-        grid_sync(lbar, lep, cpg);
+        uint32_t cnt_cur = grid_sync(lbar, lep, cpg, loc.ctl + sweep % 3u);  // this sweep's frontier size
         if (r > 0 && gtid == 0) me.inbox_cnt[pin ^ 1u] = 0;  // refilled only in round r+1
 
         // ---- 2. local sweeps to quiescence
         uint32_t nmsg = 0;
         for (;;) {
-            const uint32_t c_cur = sweep % 3u, c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
+            const uint32_t c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
             if (gtid == 0) loc.ctl[c_old] = 0;
-            const uint32_t cnt = ld_cg(loc.ctl + c_cur);
+            const uint32_t cnt = cnt_cur;
             const uint32_t *qc = (sweep & 1u) ? loc.q1 : loc.q0;
             uint32_t *qn = (sweep & 1u) ? loc.q0 : loc.q1;
             for (uint64_t it = gtid / SW; it < cnt; it += gsz / SW) {
@@ -174,9 +174,9 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
                     --budget;
                 }
             }
-            grid_sync(lbar, lep, cpg);
+            cnt_cur = grid_sync(lbar, lep, cpg, loc.ctl + c_nxt);
             ++sweep;
-            if (ld_cg(loc.ctl + c_nxt) == 0u) break;
+            if (cnt_cur == 0u) break;
         }
 
         // ---- 3. exchange barrier; stop after a round without messages

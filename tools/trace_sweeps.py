@@ -29,3 +29,13 @@ print(json.dumps({"sweeps": int(ns), "total_us": tot / 1e3, "work_us_mean": work
                   "frontier_mean": float(a[:, 3].mean()), "frontier_max": int(a[:, 3].max())}))
 for i in list(range(0, ns, max(1, ns // 25))):
     print(i, int(a[i, 3]), round(work[i] / 1e3, 2), round(bar[i] / 1e3, 2))
+
+buf2 = (ctypes.c_ulonglong * (4096 * 8))()
+L.eat_debug_trace2(buf2)
+b = np.frombuffer(buf2, dtype=np.uint64).reshape(-1, 8).astype(np.int64)[:ns]
+print("warp 0 of CTA 0 (frontier entry 0): ns from its start: [h0 loads, h0 relaxed, h0 ballot, h1 loads, h1 relaxed, h1 ballot]; sweep start->entry start")
+for i in list(range(0, ns, max(1, ns // 25))):
+    r = b[i]
+    if r[0] == 0:
+        continue
+    print(i, [int(v - r[0]) if v else None for v in r[1:7]], int(r[0] - a[i, 0]))
