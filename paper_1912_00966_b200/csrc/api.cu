@@ -316,8 +316,8 @@ eat_status upload(eat_handle *h) {
     CUDA_TRY(cudaMalloc(&h->gw.q1, n * 4ull));
     CUDA_TRY(cudaMalloc(&h->gw.stamp, n * 4ull));
     CUDA_TRY(cudaMalloc(&h->gw.bm, 3 * W * 4ull));
-    CUDA_TRY(cudaMalloc(&h->gw.ctl, 16 * 4));
-    CUDA_TRY(cudaMemset(h->gw.ctl, 0, 16 * 4));
+    CUDA_TRY(cudaMalloc(&h->gw.ctl, eat::kCtlWords * 4));
+    CUDA_TRY(cudaMemset(h->gw.ctl, 0, eat::kCtlWords * 4));
     CUDA_TRY(cudaMalloc(&h->d_out1, n * 4ull));
     CUDA_TRY(cudaMallocHost(&h->h_out1, n * 4ull + 64));
     CUDA_TRY(cudaMalloc(&h->d_q1, 2 * 4));

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 1) k_query_async(DevIndex ix, A
     __shared__ uint32_t s_cnt[2], s_more[2];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
     const uint64_t gtid = uint64_t(c) * kAsyncThreads + tid, gsz = uint64_t(P) * kAsyncThreads;
-    uint32_t *bar = w.ctl + 4;  // monotonic barrier counter (zeroed per launch)
+    uint32_t *bar = w.ctl + kBarWord;  // monotonic barrier counter (zeroed per launch)
     uint32_t bar_epoch = 0;
 
     // ---- init (Algorithm 2)
@@ -231,8 +231,8 @@ cudaError_t async_alloc(AsyncWork &w, uint32_t n, uint32_t max_parts) {
     if ((e = cudaMalloc(&w.inflag, n * 4ull + 4)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&w.inbox, 2ull * n * 4 + 4)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&w.inbox_cnt, 2ull * max_parts * 4 + 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&w.ctl, 16 * 4)) != cudaSuccess) return e;
-    return cudaMemset(w.ctl, 0, 16 * 4);
+    if ((e = cudaMalloc(&w.ctl, kCtlWords * 4)) != cudaSuccess) return e;
+    return cudaMemset(w.ctl, 0, kCtlWords * 4);
 }
 
 void async_free(AsyncWork &w) {
@@ -267,7 +267,7 @@ cudaError_t launch_query_async(const DevIndex &ix, const AsyncWork &w, uint32_t 
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_async, kAsyncThreads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    e = cudaMemsetAsync(w.ctl + 4, 0, 2 * sizeof(uint32_t), st);
+    e = cudaMemsetAsync(w.ctl + kBarWord, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     DevIndex ixc = ix;
     AsyncWork wc = w;

@@ -12,7 +12,7 @@ struct AsyncWork {
     uint32_t *inflag = nullptr;     // [n] "message pending" flags
     uint32_t *inbox = nullptr;      // [2][n] per-round-parity inboxes; owner c's region starts at c*span
     uint32_t *inbox_cnt = nullptr;  // [2][P] inbox fill counts
-    uint32_t *ctl = nullptr;        // [16]: 0-2 message counters (rotating), 4 grid barrier counter, 8 rounds, 9 sweeps
+    uint32_t *ctl = nullptr;        // [kCtlWords]: 0-2 message counters (rotating), 8 rounds, 9 sweeps, kBarWord grid barrier
 };
 
 cudaError_t async_alloc(AsyncWork &w, uint32_t n, uint32_t max_parts);

@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
     const uint32_t W = (n + 31u) / 32u;
     const uint64_t gtid = blockIdx.x * uint64_t(kGridThreads) + threadIdx.x;
     const uint64_t gsz = uint64_t(gridDim.x) * kGridThreads;
-    uint32_t *bar = w.ctl + 4;  // monotonic barrier counter (zeroed per launch)
+    uint32_t *bar = w.ctl + kBarWord;  // monotonic barrier counter (zeroed per launch)
     uint32_t bar_epoch = 0;
     // Initialize (Algorithm 2)
     for (uint64_t i = gtid; i < n; i += gsz) {
@@ -739,7 +739,7 @@ cudaError_t launch_grid_sw(const DevIndex &ix, const GridWork &w, uint32_t s, ui
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     per_sm = std::min(per_sm, grid_ctas_per_sm());
     dim3 grid(unsigned(sms * per_sm)), block(kGridThreads);
-    e = cudaMemsetAsync(w.ctl + 4, 0, 2 * sizeof(uint32_t), st);
+    e = cudaMemsetAsync(w.ctl + kBarWord, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     DevIndex ixc = ix;
     GridWork wc = w;

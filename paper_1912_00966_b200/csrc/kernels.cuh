@@ -27,13 +27,19 @@ struct DevIndex {
     const uint32_t *perm;       // [n] caller id -> internal id
 };
 
+// Control-word blocks (ctl) of the persistent kernels: kCtlWords words; the
+// grid-barrier counter sits alone on the second 128-byte line (kBarWord) so
+// its polling does not contend with the frontier counters' atomics.
+constexpr uint32_t kCtlWords = 64;
+constexpr uint32_t kBarWord = 32;
+
 // Scratch of the grid-wide persistent single-query kernel.
 struct GridWork {
     uint32_t *arr;       // [n] arrival times, internal ids
     uint32_t *q0, *q1;   // [n] frontier worklists (ping-pong)
     uint32_t *stamp;     // [n] "queued for sweep k" stamps (dedup)
     uint32_t *bm;        // [3*W] rotating active bitmaps (full-sweep schedule)
-    uint32_t *ctl;       // [16] control words: 0-2 rotating counters, 4 grid barrier counter, 8 sweeps, 11-13 window base
+    uint32_t *ctl;       // [kCtlWords]: 0-2 rotating counters, 8 sweeps, 11-13 window base, kBarWord grid barrier
 };
 
 enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2, kSchedConn = 3, kSchedBitmap = 4 };

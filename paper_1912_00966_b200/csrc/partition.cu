@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
     const uint32_t n = ix.n;
     const uint64_t gtid = blockIdx.x * uint64_t(kPartThreads) + threadIdx.x;
     const uint64_t gsz = uint64_t(gridDim.x) * kPartThreads;
-    uint32_t *bar = w.ctl + 4;  // monotonic barrier counter (zeroed per launch)
+    uint32_t *bar = w.ctl + kBarWord;  // monotonic barrier counter (zeroed per launch)
     uint32_t bar_epoch = 0;
     if (first) {
         for (uint64_t i = gtid; i < n; i += gsz) {
@@ -166,8 +166,8 @@ cudaError_t part_alloc(PartWork &w, uint32_t n) {
     if ((e = cudaMalloc(&w.q0, n * 4ull + 4)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&w.q1, n * 4ull + 4)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&w.stamp, n * 4ull + 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&w.ctl, 16 * 4)) != cudaSuccess) return e;
-    if ((e = cudaMemset(w.ctl, 0, 16 * 4)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&w.ctl, kCtlWords * 4)) != cudaSuccess) return e;
+    if ((e = cudaMemset(w.ctl, 0, kCtlWords * 4)) != cudaSuccess) return e;
     if ((e = cudaMallocHost(&w.h_flag, 64)) != cudaSuccess) return e;
     return cudaSuccess;
 }
@@ -182,7 +182,7 @@ void part_free(PartWork &w) {
 
 cudaError_t launch_part_round(const DevIndex &ix, const PartWork &w, uint32_t lo, uint32_t hi, int subwarp,
                               bool first, uint32_t s, uint32_t t_s, cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(w.ctl + 4, 0, 2 * sizeof(uint32_t), st);
+    cudaError_t e = cudaMemsetAsync(w.ctl + kBarWord, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     switch (subwarp) {
         case 0: return launch_round_sw<8>(ix, w, lo, hi, first, s, t_s, st);

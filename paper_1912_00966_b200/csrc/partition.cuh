@@ -19,7 +19,7 @@ struct PartWork {
     uint32_t *arr = nullptr;     // [n+1]: e[] replica + exchange flag word at [n]
     uint32_t *prev = nullptr;    // [n]: e[] as contributed to the last exchange
     uint32_t *q0 = nullptr, *q1 = nullptr, *stamp = nullptr;  // [n] local worklists + dedup stamps
-    uint32_t *ctl = nullptr;     // [16] counters / barrier / sweeps / stamp base
+    uint32_t *ctl = nullptr;     // [kCtlWords] counters / sweeps / stamp base, kBarWord grid barrier
     uint32_t *h_flag = nullptr;  // pinned: flag word after exchange
     uint32_t n = 0;
     uint32_t h_sweeps = 0;       // sweeps of the last query (host copy)

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
     const PeerPart me = ctx.part[p];
     const uint32_t n = ix.n, lo = me.lo, hi = me.hi, own = hi - lo;
     const uint64_t gtid = uint64_t(crank) * kPeerThreads + threadIdx.x, gsz = uint64_t(cpg) * kPeerThreads;
-    uint32_t *lbar = loc.ctl + 4;  // the group's monotonic barrier counter (zeroed per launch)
+    uint32_t *lbar = loc.ctl + kBarWord;  // the group's monotonic barrier counter (zeroed per launch)
     uint32_t lep = 0;
     const bool leader = crank == 0;
     const uint32_t rbase = ld_cg(loc.ctl + 10);  // absolute round of this query's round 0 (slots, parity)
@@ -240,8 +240,8 @@ cudaError_t peer_local_alloc(PeerLocal &l, uint32_t n) {
     if ((e = cudaMalloc(&l.q0, n * 4ull + 4)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&l.q1, n * 4ull + 4)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&l.stamp, n * 4ull + 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&l.ctl, 16 * 4)) != cudaSuccess) return e;
-    return cudaMemset(l.ctl, 0, 16 * 4);
+    if ((e = cudaMalloc(&l.ctl, kCtlWords * 4)) != cudaSuccess) return e;
+    return cudaMemset(l.ctl, 0, kCtlWords * 4);
 }
 
 void peer_local_free(PeerLocal &l) {
@@ -256,7 +256,7 @@ cudaError_t peer_query(const DevIndex *d_ix, const PeerCtx &ctx, const PeerCtx *
                        uint32_t *d_out, cudaStream_t st) {
     cudaError_t e;
     for (uint32_t g = 0; g < ctx.groups; ++g)  // group barrier counters restart at 0
-        if ((e = cudaMemsetAsync(h_loc[g].ctl + 4, 0, sizeof(uint32_t), st)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(h_loc[g].ctl + kBarWord, 0, sizeof(uint32_t), st)) != cudaSuccess) return e;
     switch (subwarp) {
         case 1: e = launch_peer_sw<1>(d_ix, ctx, d_ctx, d_loc, s, t_s, st); break;
         case 2: e = launch_peer_sw<2>(d_ix, ctx, d_ctx, d_loc, s, t_s, st); break;

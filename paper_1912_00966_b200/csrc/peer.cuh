@@ -47,7 +47,7 @@ struct PeerCtx {
 // Per partition run by this launch (memory of the launching device).
 struct PeerLocal {
     uint32_t *q0, *q1, *stamp;  // [n] local frontier worklists + dedup stamps
-    uint32_t *ctl;              // [16]: 0-2 frontier counters, 4 group barrier counter, 8 sweeps, 9 rounds, 10 round base
+    uint32_t *ctl;              // [kCtlWords]: 0-2 frontier counters, 8 sweeps, 9 rounds, 10 round base, kBarWord group barrier
 };
 
 // Bytes of one exchange block (offsets below are identical on every rank).
