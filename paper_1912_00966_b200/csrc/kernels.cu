@@ -558,7 +558,11 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
             const uint32_t cnt = cnt_cur;
             const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
             uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
-            const uint32_t lane = uint32_t(gtid % SW);
+            // a warp per frontier vertex; when the frontier outnumbers the
+            // warps, half-warps, so two vertices' dependent chains overlap
+            // (metro -5 %, country -7 %; quarter-warps lose)
+            const uint32_t sw = (SW == 32 && cnt > uint32_t(gsz >> 5)) ? 16u : uint32_t(SW);
+            const uint32_t lane = uint32_t(gtid & (sw - 1u));
             // continuation: a sub-warp that lowers e[v] relaxes v's types itself
             // in this sweep (up to ix.cont_budget extra vertices per frontier
             // vertex, default 1) instead of queueing v for the next sweep: a
@@ -566,8 +570,8 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
             // so a later lowering by anyone still queues it (chaotic relaxation
             // converges to the same fixpoint)
             const uint32_t wl = threadIdx.x & 31u;
-            const unsigned smask = SW == 32 ? 0xFFFFFFFFu : (((1u << SW) - 1u) << (wl & ~(SW - 1u)));
-            for (uint64_t it = gtid / SW; it < cnt; it += gsz / SW) {
+            const unsigned smask = sw == 32u ? 0xFFFFFFFFu : (((1u << sw) - 1u) << (wl & ~(sw - 1u)));
+            for (uint64_t it = gtid / sw; it < cnt; it += gsz / sw) {
 #ifdef EAT_EXP_TRACE
                 const bool tr0 = gtid == 0 && it == 0 && sweep < 4096;
                 uint32_t hop = 0;
@@ -582,7 +586,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
                     if (tr0 && hop < 2) g_trace2[sweep * 8 + 1 + hop * 3] = gtimer_dep(eu + p1);
 #endif
                     uint32_t cv = kNone;
-                    for (uint32_t t = p0 + lane; t < p1; t += SW) {
+                    for (uint32_t t = p0 + lane; t < p1; t += sw) {
                         const uint32_t v = relax_type_global(ix, t, eu, w.arr);
                         if (v == kNone) continue;
                         if (budget > 0 && cv == kNone) cv = v;

@@ -57,27 +57,29 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
     const uint32_t base = ld_cg(w.ctl + 10);
     bool remote = false;
     uint32_t sweep = 0;
-    const uint32_t lane = uint32_t(gtid % SW);
     const uint32_t wl = threadIdx.x & 31u;
-    const unsigned smask = SW == 32 ? 0xFFFFFFFFu : (((1u << SW) - 1u) << (wl & ~(SW - 1u)));
     for (;;) {
         const uint32_t c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
         if (gtid == 0) w.ctl[c_old] = 0;
         const uint32_t cnt = cnt_cur;
+        // half-warps per vertex when the frontier outnumbers the warps (as kernels.cu)
+        const uint32_t sw = (SW == 32 && cnt > uint32_t(gsz >> 5)) ? 16u : uint32_t(SW);
+        const uint32_t lane = uint32_t(gtid & (sw - 1u));
+        const unsigned smask = sw == 32u ? 0xFFFFFFFFu : (((1u << sw) - 1u) << (wl & ~(sw - 1u)));
         const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
         uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
         const uint32_t stamp = base + sweep + 1u;
         // continuation as in the grid frontier kernel (kernels.cu): an owned
         // vertex lowered by this sub-warp is relaxed by it in the same sweep
         // (up to ix.cont_budget extra vertices per frontier vertex)
-        for (uint64_t it = gtid / SW; it < cnt; it += gsz / SW) {
+        for (uint64_t it = gtid / sw; it < cnt; it += gsz / sw) {
             uint32_t x = ld_cg(qc + it);
             uint32_t budget = ix.cont_budget;
             for (;;) {
                 const uint32_t eu = ld_cg(w.arr + x);
                 const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
                 uint32_t cv = kNone;
-                for (uint32_t t = p0 + lane; t < p1; t += SW) {
+                for (uint32_t t = p0 + lane; t < p1; t += sw) {
                     const uint32_t v = relax_type_global(ix, t, eu, w.arr);
                     if (v == kNone) continue;
                     if (v >= lo && v < hi) {

@@ -105,9 +105,7 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
     }
     grid_sync(lbar, lep, cpg);
 
-    const uint32_t lane = uint32_t(gtid % SW);
     const uint32_t wl = threadIdx.x & 31u;
-    const unsigned smask = SW == 32 ? 0xFFFFFFFFu : (((1u << SW) - 1u) << (wl & ~(SW - 1u)));
     uint32_t sweep = 0, r = 0;
     for (;; ++r) {
         const uint32_t ra = rbase + r, pin = ra & 1u;
@@ -134,16 +132,20 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
             const uint32_t c_nxt = (sweep + 1u) % 3u, c_old = (sweep + 2u) % 3u;
             if (gtid == 0) loc.ctl[c_old] = 0;
             const uint32_t cnt = cnt_cur;
+            // half-warps per vertex when the frontier outnumbers the warps (as kernels.cu)
+            const uint32_t sw = (SW == 32 && cnt > uint32_t(gsz >> 5)) ? 16u : uint32_t(SW);
+            const uint32_t lane = uint32_t(gtid & (sw - 1u));
+            const unsigned smask = sw == 32u ? 0xFFFFFFFFu : (((1u << sw) - 1u) << (wl & ~(sw - 1u)));
             const uint32_t *qc = (sweep & 1u) ? loc.q1 : loc.q0;
             uint32_t *qn = (sweep & 1u) ? loc.q0 : loc.q1;
-            for (uint64_t it = gtid / SW; it < cnt; it += gsz / SW) {
+            for (uint64_t it = gtid / sw; it < cnt; it += gsz / sw) {
                 uint32_t x = ld_cg(qc + it);
                 uint32_t budget = ix.cont_budget;
                 for (;;) {
                     const uint32_t eu = ld_cg(me.arr + x);
                     const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
                     uint32_t cv = kNone;
-                    for (uint32_t t = p0 + lane; t < p1; t += SW) {
+                    for (uint32_t t = p0 + lane; t < p1; t += sw) {
                         uint32_t cand;
                         const uint32_t v = relax_type_global<true>(ix, t, eu, me.arr, &cand);
                         if (v == kNone) continue;
