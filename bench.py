@@ -463,7 +463,8 @@ def run_gpu(args):
             "config": {"workload": "city_batch_10k (BASELINE configs[2]; 10k queries per GPU)",
                        "stops": tt.num_vertices, "edges": st0["num_edges"], "connections": tt.num_connections,
                        "types": st0["num_types"], "queries_per_gpu": nq, "parallelism": f"query-sharded x{world}",
-                       "l2": "flushed (256 MiB write) between timed steps", "kernel": st0["kernel_name"],
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "kernel": "cta (batched)" if st0["cta_grid"] > 0 else "per-query " + st0["kernel_name"],
                        "subtrips": args.subtrips, "window_s": 1800, "cta_threads": 256,
                        "shortcuts": st0["num_shortcuts"]},
             "connections_resolved_per_s": resolved / (tot_ms / 1e3),

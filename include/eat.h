@@ -82,7 +82,7 @@ enum {
 
 /* eat_build_opts.kernel: relaxation schedule for single queries. */
 enum {
-    EAT_KERNEL_AUTO = 0,          /* CTA kernel when arr fits shared memory, else FRONTIER */
+    EAT_KERNEL_AUTO = 0,          /* single queries: CTA kernel for graphs of <= 2048 stops, else FRONTIER; batches: CTA when e[] fits shared memory */
     EAT_KERNEL_FRONTIER = 1,      /* grid-wide persistent kernel, worklist frontier, global arr */
     EAT_KERNEL_FULL_SWEEP = 2,    /* grid-wide persistent kernel, every type every sweep, active bitmap */
     EAT_KERNEL_CTA = 3,           /* one CTA per query, arr in shared memory */

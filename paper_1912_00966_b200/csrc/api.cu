@@ -382,6 +382,9 @@ eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_
     return EAT_OK;
 }
 
+// Largest graph whose single queries AUTO runs on the one-CTA kernel.
+constexpr uint32_t kAutoCtaMaxVertices = 2048;
+
 eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     h->cta_grid = eat::cta_grid_size(h->hx.n, int(h->cta_threads), h->arr16);
     h->st.smem_vertices_max = 0;
@@ -392,9 +395,13 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     h->st.smem_vertices_max = uint32_t(avail * 32 / (4 * 32 + 2 * 4));
     uint32_t k = requested;
     const bool async_ok = eat::async_parts(h->hx.n) > 0;
-    // AUTO: the CTA kernel when e[] fits shared memory, else the grid frontier
-    // kernel (measured faster than ASYNC on metro/country)
-    if (k == EAT_KERNEL_AUTO) k = h->cta_grid > 0 ? EAT_KERNEL_CTA : EAT_KERNEL_FRONTIER;
+    // AUTO for single queries: the one-CTA kernel for small graphs (tiny:
+    // 0.08 vs 0.10 ms), else the grid frontier kernel (city 0.45 vs 0.64 ms,
+    // and the only choice once e[] exceeds shared memory; faster than ASYNC
+    // on metro/country).  Batches always use the CTA kernel
+    // when e[] fits (throughput).
+    if (k == EAT_KERNEL_AUTO)
+        k = (h->cta_grid > 0 && h->hx.n <= kAutoCtaMaxVertices) ? EAT_KERNEL_CTA : EAT_KERNEL_FRONTIER;
     if (k == EAT_KERNEL_CTA && h->cta_grid == 0)
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
     if (k == EAT_KERNEL_ASYNC && !async_ok)
