@@ -367,10 +367,13 @@ def run_gpu(args):
     tot_ms = _max_over_ranks(tot_ms, dev)
     value = world * nq * args.steps / (tot_ms / 1e3)
 
-    # ---- the same batch without sub-trip shortcuts (plain Cluster-AP index)
+    # ---- the same batch with other sub-trip settings: none (plain Cluster-AP
+    # index) and the paper's scheme 2 (r = sqrt(average trip length))
     variants = {}
-    if args.subtrips:
-        eng0 = Engine.from_timetable(tt, device=dev, kernel="auto", subtrips=0)
+    for st_alt, key in ((0, "no_subtrips_queries_per_s_per_gpu"), (2, "paper_scheme2_queries_per_s_per_gpu")):
+        if st_alt == args.subtrips:
+            continue
+        eng0 = Engine.from_timetable(tt, device=dev, kernel="auto", subtrips=st_alt)
         for _ in range(2):
             eng0.query_many_device(d_src, d_ts, d_out, stream=stream)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -383,7 +386,7 @@ def run_gpu(args):
                 b.record(stream)
             b.synchronize()
             ms0 += a.elapsed_time(b)
-        variants["no_subtrips_queries_per_s_per_gpu"] = nq * 3 / (ms0 / 1e3)
+        variants[key] = nq * 3 / (ms0 / 1e3)
         eng0.close()
 
     # ---- e2e through the public API with host buffers: pinned host queries
@@ -494,8 +497,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-queries", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--subtrips", type=int, default=2,
-                    help="sub-trip shortcut scheme (PAPER.md:342-354): 0 off, 1 sqrt(k) per trip, 2 sqrt(avg)")
+    ap.add_argument("--subtrips", type=int, default=3,
+                    help="sub-trip shortcuts (PAPER.md:342-354): 0 off, 1 r=sqrt(k) per trip, 2 r=sqrt(avg) "
+                         "(the paper's scheme 2), >=3 fixed r (default 3: +3 %% q/s over scheme 2 on B200, "
+                         "profiles/r01_sweep_subtrips_r.jsonl)")
     ap.add_argument("--workload", default="city_batch", choices=["city_batch"] + sorted(SINGLE_WORKLOADS))
     ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "peer"],
                     help="country_part: per-round NCCL min-allreduce of e[] (BASELINE configs[4]) or the in-kernel "
