@@ -137,7 +137,8 @@ typedef struct eat_build_opts {
                                      (occupancy knob, tools/sweep_cta.py) */
     uint32_t subtrips;            /* sub-trip shortcuts (needs tt->trip): 0 off;
                                      1 = r = round(sqrt(k)) per trip of k connections;
-                                     2 = r = round(sqrt(average trip length)); >= 3: r itself.
+                                     2 = r = round(sqrt(average trip length)); >= 3: r itself;
+                                     EAT_SUBTRIPS_HIER + r (r >= 2): blocks of r, r^2, ... (ours).
                                      Arrival times are unchanged; sweeps (hops) drop. */
     uint32_t arr_bits;            /* batched CTA kernel e[] in shared memory: 0/16 -> uint16 offsets from t_s
                                      (twice the queries per SM; a query whose arrivals pass t_s + 65534 s is
@@ -160,6 +161,7 @@ typedef struct eat_build_opts {
 } eat_build_opts;
 
 #define EAT_CONT_NONE 0xFFFFFFFFu
+#define EAT_SUBTRIPS_HIER 1000u  /* eat_build_opts.subtrips: hierarchical sub-trips, base r = value - 1000 */
 #define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */
 
 typedef struct eat_handle eat_handle;

@@ -255,17 +255,35 @@ int make_subtrips(uint64_t m, const uint32_t *u, const uint32_t *v, const uint32
     st.trips = ntrips;
     st.chained = n_ok.load();
     const double avg = st.chained ? double(sum_len.load()) / double(st.chained) : 0.0;
-    const uint32_t r_global = scheme == 2 ? uint32_t(std::lround(std::sqrt(avg))) : (scheme >= 3 ? scheme : 0);
+    // scheme >= EAT_SUBTRIPS_HIER: hierarchical blocks of r, r^2, ... (ours)
+    const bool hier = scheme >= EAT_SUBTRIPS_HIER;
+    const uint32_t r_global = hier ? scheme - EAT_SUBTRIPS_HIER
+                              : scheme == 2 ? uint32_t(std::lround(std::sqrt(avg))) : (scheme >= 3 ? scheme : 0);
     st.r_global = r_global;
-    // emit shortcuts (count first, then fill, in trip order)
     auto r_of = [&](uint64_t k) -> uint64_t { return scheme == 1 ? uint64_t(std::llround(std::sqrt(double(k)))) : r_global; };
+    // Blocks [i, j] of one trip of k connections that get a shortcut: aligned
+    // blocks of r; hierarchical: also of r^2, r^3, ... up to the
+    // first size covering the trip, skipping blocks equal to a smaller level's.
+    auto for_blocks = [&](uint64_t k, auto &&emit) {
+        const uint64_t r = r_of(k);
+        if (r < 2) return;
+        uint64_t prev = 1;
+        for (uint64_t B = r;; prev = B, B *= r) {
+            for (uint64_t i = 0; i < k; i += B) {
+                const uint64_t j = std::min(k, i + B) - 1;
+                if (j > i && j - i + 1 > prev) emit(i, j);
+            }
+            if (!hier || B >= k) break;
+        }
+    };
+    // emit shortcuts (count first, then fill, in trip order)
     std::vector<uint64_t> cnt(ntrips + 1, 0);
     parallel_chunks(ntrips, [&](uint64_t lo, uint64_t hi) {
         for (uint64_t t = lo; t < hi; ++t) {
             if (!ok[t]) continue;
-            const uint64_t k = tptr[t + 1] - tptr[t], r = r_of(k);
-            if (r < 2) continue;
-            cnt[t + 1] = k / r + ((k % r) >= 2 ? 1 : 0);
+            uint64_t c = 0;
+            for_blocks(tptr[t + 1] - tptr[t], [&](uint64_t, uint64_t) { ++c; });
+            cnt[t + 1] = c;
         }
     });
     for (uint64_t t = 0; t < ntrips; ++t) cnt[t + 1] += cnt[t];
@@ -282,18 +300,16 @@ int make_subtrips(uint64_t m, const uint32_t *u, const uint32_t *v, const uint32
     parallel_chunks(ntrips, [&](uint64_t lo, uint64_t hi) {
         for (uint64_t t = lo; t < hi; ++t) {
             if (!ok[t] || cnt[t + 1] == cnt[t]) continue;
-            const uint64_t a = tptr[t], k = tptr[t + 1] - a, r = r_of(k);
+            const uint64_t a = tptr[t], k = tptr[t + 1] - a;
             uint64_t o = m + cnt[t];
-            for (uint64_t i = 0; i < k; i += r) {
-                const uint64_t j = std::min(k, i + r) - 1;  // sub-trip = connections i..j
-                if (j == i) continue;
+            for_blocks(k, [&](uint64_t i, uint64_t j) {  // sub-trip = connections i..j
                 const uint64_t ci = order[a + i], cj = order[a + j];
                 U[o] = u[ci];
                 V[o] = v[cj];
                 D[o] = dep[ci];
                 L[o] = dep[cj] + dur[cj] - dep[ci];
                 ++o;
-            }
+            });
         }
     });
     return EAT_OK;

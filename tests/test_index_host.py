@@ -232,21 +232,29 @@ def _expected_shortcuts(tt, scheme):
         if ok and len(idx) >= 2:
             trips.append(idx)
             lens.append(len(idx))
-    rg = round(math.sqrt(sum(lens) / len(lens))) if scheme == 2 else scheme
+    hier = scheme >= 1000  # EAT_SUBTRIPS_HIER + r: blocks of r, r^2, ... (ours, not the paper's)
+    rg = round(math.sqrt(sum(lens) / len(lens))) if scheme == 2 else (scheme - 1000 if hier else scheme)
     for idx in trips:
         k = len(idx)
         r = round(math.sqrt(k)) if scheme == 1 else rg
         if r < 2:
             continue
-        for i in range(0, k, r):
-            j = min(k, i + r) - 1
+        blocks = set()
+        size = r
+        while True:
+            for i in range(0, k, size):
+                blocks.add((i, min(k, i + size) - 1))
+            if not hier or size >= k:
+                break
+            size *= r
+        for i, j in sorted(blocks):  # a block equal to a smaller level's counts once
             if j > i:
                 a, b = idx[i], idx[j]
                 out.append((int(tt.u[a]), int(tt.v[b]), int(tt.dur[b]) + int(tt.dep[b]) - int(tt.dep[a]), int(tt.dep[a])))
     return out
 
 
-@pytest.mark.parametrize("scheme", [1, 2, 4])
+@pytest.mark.parametrize("scheme", [1, 2, 4, 1002, 1003])
 def test_subtrip_shortcuts_and_invariance(scheme):
     """NEXT-1: the index holds the original connections
     plus exactly the paper's shortcuts, and the oracle's arrival times on the

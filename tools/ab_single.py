@@ -11,7 +11,7 @@ cfg = sys.argv[2]
 kernel = sys.argv[3] if len(sys.argv) > 3 else "auto"
 subwarp = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 tt = synth.generate(cfg)
-eng = Engine.from_timetable(tt, subtrips=2, kernel=kernel, subwarp=subwarp)
+eng = Engine.from_timetable(tt, subtrips=int(os.environ.get("EAT_AB_SUBTRIPS", "3")), kernel=kernel, subwarp=subwarp)
 o1 = torch.empty(tt.num_vertices, dtype=torch.int32, device="cuda")
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
 src, ts = synth.queries(tt, 4, 1, seed=11)
