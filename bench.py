@@ -468,7 +468,7 @@ def run_gpu(args):
                        "types": st0["num_types"], "queries_per_gpu": nq, "parallelism": f"query-sharded x{world}",
                        "l2": "flushed (256 MiB write) between timed steps",
                        "kernel": "cta (batched)" if st0["cta_grid"] > 0 else "per-query " + st0["kernel_name"],
-                       "subtrips": args.subtrips, "window_s": 1800, "cta_threads": 256,
+                       "subtrips": args.subtrips, "window_s": 1200, "cta_threads": 256,
                        "shortcuts": st0["num_shortcuts"]},
             "connections_resolved_per_s": resolved / (tot_ms / 1e3),
             "variants": variants,

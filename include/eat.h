@@ -162,7 +162,7 @@ typedef struct eat_build_opts {
 
 #define EAT_CONT_NONE 0xFFFFFFFFu
 #define EAT_SUBTRIPS_HIER 1000u  /* eat_build_opts.subtrips: hierarchical sub-trips, base r = value - 1000 */
-#define EAT_DEFAULT_WINDOW 1800u   /* seconds; chosen by tools/sweep_window.py on the city batch */
+#define EAT_DEFAULT_WINDOW 1200u   /* seconds; city batch with sub-trips r = 3: 961k q/s vs 951k at 1800 s (profiles/r01_sweep_window_r3.jsonl) */
 
 typedef struct eat_handle eat_handle;
 
