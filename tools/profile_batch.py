@@ -19,7 +19,7 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--single", default="")
 ap.add_argument("--subwarp", type=int, default=8)
 ap.add_argument("--window", type=int, default=0)
-ap.add_argument("--subtrips", type=int, default=2)
+ap.add_argument("--subtrips", type=int, default=3)
 a = ap.parse_args()
 tt = synth.generate(a.config)
 if a.single:
