@@ -699,9 +699,14 @@ eat_status eat_query(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *out_arr)
         e = enqueue_single(h, s, t_s, h->d_out1, h->stream);
         if (e != EAT_OK) return e;
     }
-    CUDA_TRY(cudaMemcpyAsync(h->h_out1, h->d_out1, h->hx.n * 4ull, cudaMemcpyDeviceToHost, h->stream));
+    // page-locked output: one D2H straight into it; else through the pinned stage
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, out_arr) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    CUDA_TRY(cudaMemcpyAsync(pinned ? out_arr : h->h_out1, h->d_out1, h->hx.n * 4ull, cudaMemcpyDeviceToHost,
+                             h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
-    std::memcpy(out_arr, h->h_out1, h->hx.n * 4ull);
+    if (!pinned) std::memcpy(out_arr, h->h_out1, h->hx.n * 4ull);
     return EAT_OK;
 }
 

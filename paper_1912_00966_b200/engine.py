@@ -107,8 +107,14 @@ class Engine:
         self.close()
 
     # ------------------------------------------------------------------ queries
-    def query(self, s: int, t_s: int) -> np.ndarray:
-        out = np.empty(self.num_vertices, dtype=np.uint32)
+    def query(self, s: int, t_s: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """e[] of one query, uint32 [|V|] in caller ids.  `out` may be a
+        preallocated C-contiguous uint32 array (``pinned_empty``: the device
+        writes it directly)."""
+        if out is None:
+            out = np.empty(self.num_vertices, dtype=np.uint32)
+        elif out.shape != (self.num_vertices,) or out.dtype != np.uint32 or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a C-contiguous uint32 array of shape ({self.num_vertices},)")
         _lib.eat_query(self._h, int(s), int(t_s), out.ctypes.data)
         return out
 

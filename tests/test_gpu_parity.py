@@ -440,3 +440,23 @@ def test_peer_exchange_two_processes():
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert r.returncode == 0, r.stderr[-2000:]
     assert sorted(d["rank"] for d in lines) == [0, 1] and all(d["parity"] for d in lines), lines
+
+
+def test_query_into_caller_buffers():
+    """eat_query writes a page-locked caller buffer directly and a pageable one
+    through the pinned stage; both equal the oracle."""
+    from paper_1912_00966_b200 import pinned_empty
+
+    tt = synth.generate("tiny")
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    for kernel in ("cta", "frontier"):
+        eng = Engine.from_timetable(tt, kernel=kernel)
+        pin = pinned_empty((tt.num_vertices,))
+        page = np.zeros(tt.num_vertices, np.uint32)
+        for s, t_s in [synth.SINGLE_QUERY, (9, 50000)]:
+            want = csa.query(s, t_s)
+            assert eng.query(s, t_s, out=pin) is pin and np.array_equal(pin, want)
+            assert eng.query(s, t_s, out=page) is page and np.array_equal(page, want)
+        with pytest.raises(ValueError):
+            eng.query(0, 0, out=np.zeros(3, np.uint32))
+        eng.close()

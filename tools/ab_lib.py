@@ -12,7 +12,8 @@ d_src = torch.tensor(src.astype(np.int32), device="cuda")
 d_ts = torch.tensor(ts.astype(np.int32), device="cuda")
 out = torch.empty((src.size, tt.num_vertices), dtype=torch.int32, device="cuda")
 subtrips = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-eng = Engine.from_timetable(tt, subtrips=subtrips, window=int(os.environ.get("EAT_AB_WINDOW", "0")))
+eng = Engine.from_timetable(tt, subtrips=subtrips, window=int(os.environ.get("EAT_AB_WINDOW", "0")),
+                            cta_threads=int(os.environ.get("EAT_AB_THREADS", "0")))
 for _ in range(3):
     eng.query_many_device(d_src, d_ts, out)
 torch.cuda.synchronize()
@@ -28,5 +29,5 @@ a.record()
 for _ in range(20):
     eng.query_device(*synth.SINGLE_QUERY, o1)
 b.record(); b.synchronize()
-print(json.dumps({"lib": os.path.basename(sys.argv[1]), "subtrips": subtrips, "window": int(os.environ.get("EAT_AB_WINDOW", "0")), "shortcuts": eng.stats()["num_shortcuts"], "batch_ms_med": float(np.median(ms)), "qps": src.size / float(np.median(ms)) * 1e3,
+print(json.dumps({"lib": os.path.basename(sys.argv[1]), "subtrips": subtrips, "window": int(os.environ.get("EAT_AB_WINDOW", "0")), "threads": int(os.environ.get("EAT_AB_THREADS", "0")), "shortcuts": eng.stats()["num_shortcuts"], "batch_ms_med": float(np.median(ms)), "qps": src.size / float(np.median(ms)) * 1e3,
                   "single_ms": a.elapsed_time(b) / 20, "crc": int(out[::97].sum().item()), "crc1": int(o1.sum().item())}), flush=True)
