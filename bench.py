@@ -36,6 +36,7 @@ sys.path.insert(0, ROOT)
 METRIC = "EAT queries/s"
 UNIT = "queries/s"
 QUERIES_PER_RANK = (1000, 10)  # sources x times
+L2_READ_GBS = 17805.0  # measured L2-resident read bandwidth, 32 MiB working set (profiles/r01_ncu_summary.md)
 
 
 def _dist():
@@ -451,7 +452,11 @@ def run_gpu(args):
                 traffic = json.load(f).get("dram_bytes_per_launch")
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src, "kernel": "k_query_cta",
-                "algorithmic_bytes_per_launch": alg_bytes, "counters": cnt}
+                "algorithmic_bytes_per_launch": alg_bytes, "counters": cnt,
+                # the index is L2-resident: the same bytes against the measured
+                # L2-resident read bandwidth (tools/l2_bw.py, profiles/r01_ncu_summary.md)
+                "l2": {"peak": L2_READ_GBS, "frac": achieved / L2_READ_GBS,
+                       "note": "kernel is issue-bound (ncu: IPC 2.44 of 4), not bandwidth-bound"}}
     except Exception as exc:  # keep the bench line even if accounting fails
         roof = {"bound": "hbm", "achieved": None, "peak": _peaks()[0], "unit": "GB/s", "frac": None,
                 "traffic": None, "error": repr(exc)}

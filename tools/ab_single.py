@@ -11,7 +11,8 @@ cfg = sys.argv[2]
 kernel = sys.argv[3] if len(sys.argv) > 3 else "auto"
 subwarp = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 tt = synth.generate(cfg)
-eng = Engine.from_timetable(tt, subtrips=int(os.environ.get("EAT_AB_SUBTRIPS", "3")), kernel=kernel, subwarp=subwarp)
+eng = Engine.from_timetable(tt, subtrips=int(os.environ.get("EAT_AB_SUBTRIPS", "3")), kernel=kernel, subwarp=subwarp,
+                            continuation=int(os.environ["EAT_AB_CONT"]) if "EAT_AB_CONT" in os.environ else None)
 o1 = torch.empty(tt.num_vertices, dtype=torch.int32, device="cuda")
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
 src, ts = synth.queries(tt, 4, 1, seed=11)
@@ -30,5 +31,5 @@ for (s, t) in qs:
         ms.append(a.elapsed_time(b))
     ok = bool(np.array_equal(o1.cpu().numpy().astype(np.uint32), csa.query(s, t)))
     res[f"{s}@{t}"] = {"ms": float(np.median(ms)), "sweeps": eng.stats()["last_sweeps"], "parity": ok}
-print(json.dumps({"lib": os.path.basename(sys.argv[1]), "config": cfg, "kernel": kernel, "subwarp": subwarp,
+print(json.dumps({"lib": os.path.basename(sys.argv[1]), "config": cfg, "kernel": kernel, "subwarp": subwarp, "cont": os.environ.get("EAT_AB_CONT"),
                   "mean_ms": float(np.mean([v["ms"] for v in res.values()])), "queries": res}), flush=True)
