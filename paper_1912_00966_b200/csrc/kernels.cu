@@ -579,9 +579,9 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
 #endif
                 uint32_t x = ld_cg(qc + it);
                 uint32_t budget = ix.cont_budget;
+                uint32_t eu = ld_cg(w.arr + x);
+                uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
                 for (;;) {
-                    const uint32_t eu = ld_cg(w.arr + x);
-                    const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
 #ifdef EAT_EXP_TRACE
                     if (tr0 && hop < 2) g_trace2[sweep * 8 + 1 + hop * 3] = gtimer_dep(eu + p1);
 #endif
@@ -602,10 +602,13 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
 #endif
                     if (!cm) break;
                     const uint32_t src = __ffs(cm) - 1u;
-                    const uint32_t nx = __shfl_sync(smask, cv, src);
+                    x = __shfl_sync(smask, cv, src);
+                    // the next hop's loads go out before this hop's queue pushes
+                    eu = ld_cg(w.arr + x);
+                    p0 = __ldg(ix.type_ptr + x);
+                    p1 = __ldg(ix.type_ptr + x + 1);
                     if (cv != kNone && wl != src && atomicExch(w.stamp + cv, sweep + 1u) != sweep + 1u)
                         push_aggregated(cv, qn, w.ctl + c_nxt);
-                    x = nx;
                     --budget;
                 }
             }

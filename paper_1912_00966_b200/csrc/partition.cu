@@ -75,9 +75,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
         for (uint64_t it = gtid / sw; it < cnt; it += gsz / sw) {
             uint32_t x = ld_cg(qc + it);
             uint32_t budget = ix.cont_budget;
+            uint32_t eu = ld_cg(w.arr + x);
+            uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
             for (;;) {
-                const uint32_t eu = ld_cg(w.arr + x);
-                const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
                 uint32_t cv = kNone;
                 for (uint32_t t = p0 + lane; t < p1; t += sw) {
                     const uint32_t v = relax_type_global(ix, t, eu, w.arr);
@@ -92,10 +92,13 @@ __global__ void __launch_bounds__(kPartThreads) k_part_round(DevIndex ix, PartWo
                 const unsigned cm = __ballot_sync(smask, cv != kNone) & smask;
                 if (!cm) break;
                 const uint32_t src = __ffs(cm) - 1u;
-                const uint32_t nx = __shfl_sync(smask, cv, src);
+                x = __shfl_sync(smask, cv, src);
+                // the next hop's loads go out before this hop's queue pushes
+                eu = ld_cg(w.arr + x);
+                p0 = __ldg(ix.type_ptr + x);
+                p1 = __ldg(ix.type_ptr + x + 1);
                 if (cv != kNone && wl != src && atomicExch(w.stamp + cv, stamp) != stamp)
                     push_aggregated(cv, qn, w.ctl + c_nxt);
-                x = nx;
                 --budget;
             }
         }

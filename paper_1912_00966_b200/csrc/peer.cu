@@ -141,9 +141,9 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
             for (uint64_t it = gtid / sw; it < cnt; it += gsz / sw) {
                 uint32_t x = ld_cg(qc + it);
                 uint32_t budget = ix.cont_budget;
+                uint32_t eu = ld_cg(me.arr + x);
+                uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
                 for (;;) {
-                    const uint32_t eu = ld_cg(me.arr + x);
-                    const uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
                     uint32_t cv = kNone;
                     for (uint32_t t = p0 + lane; t < p1; t += sw) {
                         uint32_t cand;
@@ -169,10 +169,13 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
                     const unsigned cm = __ballot_sync(smask, cv != kNone) & smask;
                     if (!cm) break;
                     const uint32_t src = __ffs(cm) - 1u;
-                    const uint32_t nx = __shfl_sync(smask, cv, src);
+                    x = __shfl_sync(smask, cv, src);
+                    // the next hop's loads go out before this hop's queue pushes
+                    eu = ld_cg(me.arr + x);
+                    p0 = __ldg(ix.type_ptr + x);
+                    p1 = __ldg(ix.type_ptr + x + 1);
                     if (cv != kNone && wl != src && atomicExch(loc.stamp + cv, sweep + 1u) != sweep + 1u)
                         push_aggregated(cv, qn, loc.ctl + c_nxt);
-                    x = nx;
                     --budget;
                 }
             }
