@@ -136,7 +136,7 @@ namespace {
 void release_device(eat_handle *h) {
     if (h->host_only) return;
     cudaSetDevice(h->device);
-    void *ptrs[] = {h->d_perm,  h->gw.arr, h->gw.q0,     h->gw.q1,      h->gw.stamp,   h->gw.bm,
+    void *ptrs[] = {h->d_perm,  h->gw.arr, h->gw.q0,     h->gw.q1,      h->gw.r0,      h->gw.r1,      h->gw.stamp,   h->gw.bm,
                     h->gw.ctl,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
                     h->d_bsrc[0], h->d_bts[0], h->d_bout[0], h->d_bsrc[1], h->d_bts[1], h->d_bout[1],
                     h->d_bcounter, h->d_work, h->d_rounds1, h->d_ovf[0], h->d_ovf[1], h->d_ovf[2],
@@ -314,6 +314,8 @@ eat_status upload(eat_handle *h) {
     CUDA_TRY(cudaMalloc(&h->gw.arr, n * 4ull));
     CUDA_TRY(cudaMalloc(&h->gw.q0, n * 4ull));
     CUDA_TRY(cudaMalloc(&h->gw.q1, n * 4ull));
+    CUDA_TRY(cudaMalloc(&h->gw.r0, n * 8ull));
+    CUDA_TRY(cudaMalloc(&h->gw.r1, n * 8ull));
     CUDA_TRY(cudaMalloc(&h->gw.stamp, n * 4ull));
     CUDA_TRY(cudaMalloc(&h->gw.bm, 3 * W * 4ull));
     CUDA_TRY(cudaMalloc(&h->gw.ctl, eat::kCtlWords * 4));

@@ -203,6 +203,19 @@ __device__ __forceinline__ void push_aggregated(uint32_t v, uint32_t *q, uint32_
     q[base + __popc(am & ((1u << lane) - 1u))] = v;
 }
 
+// Warp-aggregated append of v and its type range to a worklist.
+__device__ __forceinline__ void push_aggregated(uint32_t v, uint2 rng, uint32_t *q, uint2 *qr, uint32_t *count) {
+    const unsigned am = __activemask();
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned leader = __ffs(am) - 1u;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(count, uint32_t(__popc(am)));
+    base = __shfl_sync(am, base, leader);
+    const uint32_t pos = base + __popc(am & ((1u << lane) - 1u));
+    q[pos] = v;
+    qr[pos] = rng;
+}
+
 // Relax one connection type (Algorithm 3) whose source has
 // arrival eu, against a global e[] (atomicMin).  Returns
 // the target v when this call strictly lowered e[v], else kNone; *cand_out

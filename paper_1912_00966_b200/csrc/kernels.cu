@@ -472,7 +472,10 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
     if (gtid == 0) {
         const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
         w.arr[si] = ts;
-        if (!kBitmapSched) w.q0[0] = si;
+        if (!kBitmapSched) {
+            w.q0[0] = si;
+            w.r0[0] = make_uint2(__ldg(ix.type_ptr + si), __ldg(ix.type_ptr + si + 1));
+        }
         else w.bm[si >> 5] = 1u << (si & 31u);
     }
     uint32_t cnt_cur = grid_sync(bar, bar_epoch, w.ctl + 0);  // sweep 0's frontier size (1)
@@ -558,6 +561,10 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
             const uint32_t cnt = cnt_cur;
             const uint32_t *qc = (sweep & 1u) ? w.q1 : w.q0;
             uint32_t *qn = (sweep & 1u) ? w.q0 : w.q1;
+            // queued vertices carry their type range, so a hop's type records
+            // are fetched together with e[x] instead of after type_ptr[x]
+            const uint2 *rc = (sweep & 1u) ? w.r1 : w.r0;
+            uint2 *rn = (sweep & 1u) ? w.r0 : w.r1;
             // a warp per frontier vertex; when the frontier outnumbers the
             // warps, half-warps, so two vertices' dependent chains overlap
             // (metro -5 %, country -7 %; quarter-warps lose)
@@ -580,7 +587,8 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
                 uint32_t x = ld_cg(qc + it);
                 uint32_t budget = ix.cont_budget;
                 uint32_t eu = ld_cg(w.arr + x);
-                uint32_t p0 = __ldg(ix.type_ptr + x), p1 = __ldg(ix.type_ptr + x + 1);
+                const uint2 rx = __ldcg(rc + it);
+                uint32_t p0 = rx.x, p1 = rx.y;
                 for (;;) {
 #ifdef EAT_EXP_TRACE
                     if (tr0 && hop < 2) g_trace2[sweep * 8 + 1 + hop * 3] = gtimer_dep(eu + p1);
@@ -589,8 +597,12 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
                     for (uint32_t t = p0 + lane; t < p1; t += sw) {
                         const uint32_t v = relax_type_global(ix, t, eu, w.arr);
                         if (v == kNone) continue;
-                        if (budget > 0 && cv == kNone) cv = v;
-                        else if (atomicExch(w.stamp + v, sweep + 1u) != sweep + 1u) push_aggregated(v, qn, w.ctl + c_nxt);
+                        if (budget > 0 && cv == kNone) {
+                            cv = v;
+                            continue;
+                        }
+                        const uint2 rv = make_uint2(__ldg(ix.type_ptr + v), __ldg(ix.type_ptr + v + 1));
+                        if (atomicExch(w.stamp + v, sweep + 1u) != sweep + 1u) push_aggregated(v, rv, qn, rn, w.ctl + c_nxt);
                     }
 #ifdef EAT_EXP_TRACE
                     if (tr0 && hop < 2) g_trace2[sweep * 8 + 2 + hop * 3] = gtimer_dep(cv);
@@ -607,8 +619,10 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
                     eu = ld_cg(w.arr + x);
                     p0 = __ldg(ix.type_ptr + x);
                     p1 = __ldg(ix.type_ptr + x + 1);
-                    if (cv != kNone && wl != src && atomicExch(w.stamp + cv, sweep + 1u) != sweep + 1u)
-                        push_aggregated(cv, qn, w.ctl + c_nxt);
+                    if (cv != kNone && wl != src) {
+                        const uint2 rv = make_uint2(__ldg(ix.type_ptr + cv), __ldg(ix.type_ptr + cv + 1));
+                        if (atomicExch(w.stamp + cv, sweep + 1u) != sweep + 1u) push_aggregated(cv, rv, qn, rn, w.ctl + c_nxt);
+                    }
                     --budget;
                 }
             }

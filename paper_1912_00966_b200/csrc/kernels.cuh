@@ -37,6 +37,7 @@ constexpr uint32_t kBarWord = 32;
 struct GridWork {
     uint32_t *arr;       // [n] arrival times, internal ids
     uint32_t *q0, *q1;   // [n] frontier worklists (ping-pong)
+    uint2 *r0, *r1;      // [n] type range [type_ptr[x], type_ptr[x+1]) of each queued x (frontier schedule)
     uint32_t *stamp;     // [n] "queued for sweep k" stamps (dedup)
     uint32_t *bm;        // [3*W] rotating active bitmaps (full-sweep schedule)
     uint32_t *ctl;       // [kCtlWords]: 0-2 rotating counters, 8 sweeps, 11-13 window base, kBarWord grid barrier

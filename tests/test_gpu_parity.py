@@ -406,7 +406,7 @@ def test_goal_directed_targets():
         _assert_rows(eng.query_targets(src, ts, dst), want, f"targets seed {seed}")
 
 
-@pytest.mark.parametrize("scheme", [1, 2])
+@pytest.mark.parametrize("scheme", [1, 2, 3, 1003])
 def test_subtrips_parity(scheme):
     """NEXT-1: the index with sub-trip shortcuts gives the oracle's arrival
     times of the ORIGINAL timetable (batched + single kernels)."""
