@@ -94,6 +94,8 @@ struct eat_handle {
     bool loopback = false;
     // single-query scratch
     eat::GridWork gw{};
+    std::vector<eat::GridWork> bgw;   // batched queries without shared-memory e[]: one scratch per CTA group
+    eat::GridWork *d_bgw = nullptr;
     eat::AsyncWork aw{};
     uint32_t *d_out1 = nullptr, *h_out1 = nullptr;
     uint32_t *d_q1 = nullptr;  // [2]: s, t_s for the CTA kernel
@@ -133,11 +135,35 @@ struct eat_handle {
 
 namespace {
 
+// Scratch of one grid-kernel query (bitmaps only for the bitmap schedules).
+cudaError_t gridwork_alloc(eat::GridWork &w, uint64_t n, bool bitmaps) {
+    const uint64_t W = (n + 31ull) / 32ull;
+    cudaError_t e;
+    if ((e = cudaMalloc(&w.arr, n * 4ull)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&w.q0, n * 4ull)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&w.q1, n * 4ull)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&w.r0, n * 8ull)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&w.r1, n * 8ull)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&w.stamp, n * 4ull)) != cudaSuccess) return e;
+    if (bitmaps && (e = cudaMalloc(&w.bm, 3 * W * 4ull)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&w.ctl, eat::kCtlWords * 4)) != cudaSuccess) return e;
+    return cudaMemset(w.ctl, 0, eat::kCtlWords * 4);
+}
+
+void gridwork_free(eat::GridWork &w) {
+    void *ptrs[] = {w.arr, w.q0, w.q1, w.r0, w.r1, w.stamp, w.bm, w.ctl};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    w = eat::GridWork{};
+}
+
 void release_device(eat_handle *h) {
     if (h->host_only) return;
     cudaSetDevice(h->device);
-    void *ptrs[] = {h->d_perm,  h->gw.arr, h->gw.q0,     h->gw.q1,      h->gw.r0,      h->gw.r1,      h->gw.stamp,   h->gw.bm,
-                    h->gw.ctl,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
+    gridwork_free(h->gw);
+    for (eat::GridWork &w : h->bgw) gridwork_free(w);
+    if (h->d_bgw) cudaFree(h->d_bgw);
+    void *ptrs[] = {h->d_perm,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
                     h->d_bsrc[0], h->d_bts[0], h->d_bout[0], h->d_bsrc[1], h->d_bts[1], h->d_bout[1],
                     h->d_bcounter, h->d_work, h->d_rounds1, h->d_ovf[0], h->d_ovf[1], h->d_ovf[2],
                     h->d_conns, h->d_dsrc, h->d_dts};
@@ -310,16 +336,7 @@ eat_status upload(eat_handle *h) {
     h->st.num_spill_items = s0.num_pool;
     h->st.index_bytes = h->index_bytes;
     // scratch
-    const uint64_t W = (n + 31ull) / 32ull;
-    CUDA_TRY(cudaMalloc(&h->gw.arr, n * 4ull));
-    CUDA_TRY(cudaMalloc(&h->gw.q0, n * 4ull));
-    CUDA_TRY(cudaMalloc(&h->gw.q1, n * 4ull));
-    CUDA_TRY(cudaMalloc(&h->gw.r0, n * 8ull));
-    CUDA_TRY(cudaMalloc(&h->gw.r1, n * 8ull));
-    CUDA_TRY(cudaMalloc(&h->gw.stamp, n * 4ull));
-    CUDA_TRY(cudaMalloc(&h->gw.bm, 3 * W * 4ull));
-    CUDA_TRY(cudaMalloc(&h->gw.ctl, eat::kCtlWords * 4));
-    CUDA_TRY(cudaMemset(h->gw.ctl, 0, eat::kCtlWords * 4));
+    CUDA_TRY(gridwork_alloc(h->gw, n, true));
     CUDA_TRY(cudaMalloc(&h->d_out1, n * 4ull));
     CUDA_TRY(cudaMallocHost(&h->h_out1, n * 4ull + 64));
     CUDA_TRY(cudaMalloc(&h->d_q1, 2 * 4));
@@ -383,6 +400,13 @@ eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_
     CUDA_TRY(cudaStreamSynchronize(st));
     return EAT_OK;
 }
+
+// CTA groups (queries in flight) of the batched kernel when e[] does not fit
+// shared memory: nq / 4, at most 74 (two CTAs per group); metro 256 queries
+// 1.1k q/s with one group -> 11.2k q/s with 74, country 64 queries best at 16
+// (tools/sweep_groups.py, profiles/r01_sweep_batch_groups.jsonl).
+// EAT_BATCH_GROUPS overrides.
+constexpr uint32_t kBatchGroupsMax = 74;
 
 // Largest graph whose single queries AUTO runs on the one-CTA kernel.
 constexpr uint32_t kAutoCtaMaxVertices = 2048;
@@ -755,22 +779,23 @@ eat_status launch_batch_cta(eat_handle *h, const uint32_t *d_sources, const uint
 eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
                          uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, int slot = 0) {
     if (h->cta_grid > 0) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, d_qcounter, slot, nullptr);
-    std::vector<uint32_t> hs(nq), ht(nq);
-    CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sources, nq * 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(ht.data(), d_times, nq * 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<uint32_t> inf;
-    for (uint64_t q = 0; q < nq; ++q) {
-        uint32_t *row = d_out + q * uint64_t(h->hx.n);
-        if (hs[q] >= h->hx.n || ht[q] >= EAT_INF) {
-            if (inf.empty()) inf.assign(h->hx.n, EAT_INF);
-            CUDA_TRY(cudaMemcpyAsync(row, inf.data(), h->hx.n * 4ull, cudaMemcpyHostToDevice, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-            continue;
+    // e[] in global memory: CTA groups of one launch take queries in turn
+    uint32_t groups = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(kBatchGroupsMax, nq / 4)));
+    if (const char *gv = getenv("EAT_BATCH_GROUPS")) groups = uint32_t(std::max(1, std::min(148, atoi(gv))));
+    groups = uint32_t(std::min<uint64_t>(groups, nq));
+    if (h->bgw.size() < groups) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        while (h->bgw.size() < groups) {
+            h->bgw.emplace_back();
+            CUDA_TRY(gridwork_alloc(h->bgw.back(), h->hx.n, false));
         }
-        eat_status e = enqueue_single(h, hs[q], ht[q], row, st);
-        if (e != EAT_OK) return e;
+        if (h->d_bgw) cudaFree(h->d_bgw);
+        h->d_bgw = nullptr;
+        CUDA_TRY(cudaMalloc(&h->d_bgw, h->bgw.size() * sizeof(eat::GridWork)));
+        CUDA_TRY(cudaMemcpy(h->d_bgw, h->bgw.data(), h->bgw.size() * sizeof(eat::GridWork), cudaMemcpyHostToDevice));
     }
+    CUDA_TRY(eat::launch_query_groups(h->ix, h->subwarp == 0 ? 32 : int(h->subwarp), h->bgw.data(), h->d_bgw, groups,
+                                      d_sources, d_times, nq, d_out, d_qcounter, h->d_invalid, st));
     return EAT_OK;
 }
 

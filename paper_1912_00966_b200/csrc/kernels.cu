@@ -443,15 +443,14 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
 // DESIGN.md §9).
 constexpr int kGridThreads = 1024;
 
+// One query by `nctas` co-resident CTAs (thread gtid of gsz): the whole grid
+// (k_query_grid) or one CTA group of a multi-query launch (k_query_groups).
 template <int SW, int SCHED>
-__global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, GridWork w, uint32_t s, uint32_t ts,
-                                                             uint32_t *out) {
+__device__ __forceinline__ void grid_solve(const DevIndex &ix, const GridWork &w, uint32_t s, uint32_t ts,
+                                           uint32_t *out, uint64_t gtid, uint64_t gsz, uint32_t nctas,
+                                           uint32_t *bar, uint32_t &bar_epoch) {
     const uint32_t n = ix.n;
     const uint32_t W = (n + 31u) / 32u;
-    const uint64_t gtid = blockIdx.x * uint64_t(kGridThreads) + threadIdx.x;
-    const uint64_t gsz = uint64_t(gridDim.x) * kGridThreads;
-    uint32_t *bar = w.ctl + kBarWord;  // monotonic barrier counter (zeroed per launch)
-    uint32_t bar_epoch = 0;
     // Initialize (Algorithm 2)
     for (uint64_t i = gtid; i < n; i += gsz) {
         w.arr[i] = kInf;
@@ -468,7 +467,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
         w.ctl[12] = kInf;
         w.ctl[13] = kInf;
     }
-    grid_sync(bar, bar_epoch);
+    grid_sync(bar, bar_epoch, nctas);
     if (gtid == 0) {
         const uint32_t si = __ldg(ix.perm + s);  // caller id -> internal id
         w.arr[si] = ts;
@@ -478,7 +477,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
         }
         else w.bm[si >> 5] = 1u << (si & 31u);
     }
-    uint32_t cnt_cur = grid_sync(bar, bar_epoch, w.ctl + 0);  // sweep 0's frontier size (1)
+    uint32_t cnt_cur = grid_sync(bar, bar_epoch, nctas, w.ctl + 0);  // sweep 0's frontier size (1)
 
     uint32_t sweep = 0;
     for (;;) {
@@ -684,7 +683,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
         __syncthreads();
         if (threadIdx.x == 0 && sweep < 4096) atomicMax(&g_trace[sweep * 4 + 1], gtimer());
 #endif
-        cnt_cur = grid_sync(bar, bar_epoch, w.ctl + c_nxt);  // next frontier size / improved flag
+        cnt_cur = grid_sync(bar, bar_epoch, nctas, w.ctl + c_nxt);  // next frontier size / improved flag
 #ifdef EAT_EXP_TRACE
         if (gtid == 0 && sweep < 4096) g_trace[sweep * 4 + 2] = gtimer();
 #endif
@@ -693,6 +692,48 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
     }
     for (uint64_t i = gtid; i < n; i += gsz) out[i] = ld_cg(w.arr + __ldg(ix.perm + i));
     if (gtid == 0) w.ctl[8] = sweep;
+}
+
+template <int SW, int SCHED>
+__global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, GridWork w, uint32_t s, uint32_t ts,
+                                                             uint32_t *out) {
+    uint32_t epoch = 0;  // barrier counter w.ctl[kBarWord] is zeroed per launch
+    grid_solve<SW, SCHED>(ix, w, s, ts, out, blockIdx.x * uint64_t(kGridThreads) + threadIdx.x,
+                          uint64_t(gridDim.x) * kGridThreads, gridDim.x, w.ctl + kBarWord, epoch);
+}
+
+// Batched queries when e[] does not fit shared memory (e[]
+// in global memory): the grid splits into groups of cpg CTAs; each group
+// takes queries from a global counter and solves them one after another
+// with the frontier schedule, using its own scratch (ws[g]) and barrier.
+template <int SW>
+__global__ void __launch_bounds__(kGridThreads, 1) k_query_groups(DevIndex ix, const GridWork *__restrict__ ws,
+                                                               uint32_t cpg, const uint32_t *__restrict__ src,
+                                                               const uint32_t *__restrict__ tsv, uint64_t nq,
+                                                               uint32_t *__restrict__ out,
+                                                               unsigned long long *qcounter,
+                                                               unsigned long long *invalid) {
+    const uint32_t g = blockIdx.x / cpg, crank = blockIdx.x % cpg;
+    const GridWork w = ws[g];
+    const uint64_t gtid = crank * uint64_t(kGridThreads) + threadIdx.x, gsz = uint64_t(cpg) * kGridThreads;
+    uint32_t *bar = w.ctl + kBarWord;
+    uint32_t epoch = 0;
+    for (;;) {
+        if (gtid == 0) {
+            const unsigned long long qi = atomicAdd(qcounter, 1ull);
+            w.ctl[20] = qi < nq ? uint32_t(qi) : 0xFFFFFFFFu;
+        }
+        const uint32_t q = grid_sync(bar, epoch, cpg, w.ctl + 20);  // also: the previous row is written
+        if (q == 0xFFFFFFFFu) break;
+        uint32_t *orow = out + uint64_t(q) * ix.n;
+        const uint32_t s = src[q], ts = tsv[q];
+        if (s >= ix.n || ts >= kInf) {
+            for (uint64_t i = gtid; i < ix.n; i += gsz) orow[i] = kInf;
+            if (gtid == 0) atomicAdd(invalid, 1ull);
+            continue;
+        }
+        grid_solve<SW, kSchedFrontier>(ix, w, s, ts, orow, gtid, gsz, cpg, bar, epoch);
+    }
 }
 
 template <bool COUNT, int T, int L, bool A16, bool TGT = false>
@@ -747,6 +788,30 @@ cudaError_t launch_cta_variant(const DevIndex &ix, const CtaArgs &a, cudaStream_
         case 128: return launch_cta_pair<COUNT, 128, 512>(ix, a, st);
         default: return launch_cta_pair<COUNT, 256, 512>(ix, a, st);
     }
+}
+
+template <int SW>
+cudaError_t launch_groups_sw(const DevIndex &ix, const GridWork *h_ws, const GridWork *d_ws, uint32_t groups,
+                             const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
+                             unsigned long long *qcounter, unsigned long long *invalid, cudaStream_t st) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_groups<SW>, kGridThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    per_sm = std::min(per_sm, grid_ctas_per_sm());
+    const uint32_t cpg = uint32_t(sms * per_sm) / groups;
+    if (cpg < 1) return cudaErrorInvalidConfiguration;
+    for (uint32_t g = 0; g < groups; ++g)
+        if ((e = cudaMemsetAsync(h_ws[g].ctl + kBarWord, 0, sizeof(uint32_t), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(qcounter, 0, sizeof(unsigned long long), st)) != cudaSuccess) return e;
+    DevIndex ixc = ix;
+    const GridWork *wp = d_ws;
+    uint32_t c = cpg;
+    void *args[] = {&ixc, &wp, &c, &src, &ts, &nq, &out, &qcounter, &invalid};
+    return cudaLaunchCooperativeKernel((const void *)k_query_groups<SW>, dim3(groups * cpg), dim3(kGridThreads), args,
+                                       0, st);
 }
 
 template <int SW, int SCHED>
@@ -826,6 +891,20 @@ cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint
 
 cudaError_t launch_query_cta(const DevIndex &ix, const CtaArgs &a, cudaStream_t st) {
     return (a.counters && !a.dst) ? launch_cta_variant<true>(ix, a, st) : launch_cta_variant<false>(ix, a, st);
+}
+
+cudaError_t launch_query_groups(const DevIndex &ix, int subwarp, const GridWork *h_ws, const GridWork *d_ws,
+                                uint32_t groups, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
+                                unsigned long long *qcounter, unsigned long long *invalid, cudaStream_t st) {
+    if (nq == 0) return cudaSuccess;
+    switch (subwarp) {
+        case 1: return launch_groups_sw<1>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
+        case 2: return launch_groups_sw<2>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
+        case 4: return launch_groups_sw<4>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
+        case 8: return launch_groups_sw<8>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
+        case 16: return launch_groups_sw<16>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
+        default: return launch_groups_sw<32>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
+    }
 }
 
 cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const GridWork &w, uint32_t s,

@@ -223,6 +223,30 @@ def test_metro_single_query():
             _assert_rows(e2.query(s, t_s), csa.query(s, t_s), f"metro {kernel} ({s},{t_s})")
 
 
+def test_metro_batched_groups():
+    """a12 with e[] in global memory: batched metro queries run as CTA groups
+    of one launch (several queries in flight); every row equals the oracle's,
+    invalid queries give INF rows (device path)."""
+    import torch
+
+    tt = synth.generate("metro")
+    eng = Engine.from_timetable(tt, subtrips=3)
+    assert eng.stats()["cta_grid"] == 0  # e[] exceeds shared memory
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    src, ts = synth.queries(tt, 12, 3)
+    _assert_rows(eng.query_many(src, ts), csa.query_many(src, ts), "metro batch (host)")
+    bad_s = src.astype(np.int64).copy()
+    bad_s[5] = tt.num_vertices + 3
+    d_src = torch.tensor(bad_s.astype(np.int32), device="cuda")
+    d_ts = torch.tensor(ts.astype(np.int32), device="cuda")
+    out = torch.empty((src.size, tt.num_vertices), dtype=torch.int32, device="cuda")
+    eng.query_many_device(d_src, d_ts, out)
+    got = out.cpu().numpy().astype(np.uint32)
+    assert (got[5] == INF).all()
+    keep = np.arange(src.size) != 5
+    _assert_rows(got[keep], csa.query_many(src[keep], ts[keep]), "metro batch (device)")
+
+
 # ----------------------------------------------------------------------------- edge partition
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
 def test_edge_partitioned_loopback(P):
