@@ -776,10 +776,11 @@ eat_status launch_batch_cta(eat_handle *h, const uint32_t *d_sources, const uint
     return EAT_OK;
 }
 
-eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
-                         uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, int slot = 0) {
-    if (h->cta_grid > 0) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, d_qcounter, slot, nullptr);
-    // e[] in global memory: CTA groups of one launch take queries in turn
+// Batched queries whose e[] does not fit shared memory: CTA groups of one
+// cooperative launch take queries in turn (k_query_groups); dst != NULL:
+// goal-directed, out[q] = e[dst[q]].
+eat_status launch_batch_groups(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
+                               uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, const uint32_t *d_dst) {
     uint32_t groups = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(kBatchGroupsMax, nq / 4)));
     if (const char *gv = getenv("EAT_BATCH_GROUPS")) groups = uint32_t(std::max(1, std::min(148, atoi(gv))));
     groups = uint32_t(std::min<uint64_t>(groups, nq));
@@ -795,8 +796,14 @@ eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_
         CUDA_TRY(cudaMemcpy(h->d_bgw, h->bgw.data(), h->bgw.size() * sizeof(eat::GridWork), cudaMemcpyHostToDevice));
     }
     CUDA_TRY(eat::launch_query_groups(h->ix, h->subwarp == 0 ? 32 : int(h->subwarp), h->bgw.data(), h->d_bgw, groups,
-                                      d_sources, d_times, nq, d_out, d_qcounter, h->d_invalid, st));
+                                      d_sources, d_times, nq, d_out, d_qcounter, h->d_invalid, d_dst, st));
     return EAT_OK;
+}
+
+eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
+                         uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, int slot = 0) {
+    if (h->cta_grid > 0) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, d_qcounter, slot, nullptr);
+    return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, d_qcounter, nullptr);
 }
 
 // Parallel host copy (staging -> caller memory).
@@ -843,24 +850,8 @@ eat_status eat_query_many_target_device(eat_handle *h, const uint32_t *d_sources
     CUDA_TRY(cudaSetDevice(h->device));
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     if (h->cta_grid > 0) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, h->d_counter, 0, d_dsts);
-    // e[] too large for shared memory: full single queries, then e[dst]
-    std::vector<uint32_t> hs(nq), ht(nq), hd(nq);
-    CUDA_TRY(cudaMemcpyAsync(hs.data(), d_sources, nq * 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(ht.data(), d_times, nq * 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(hd.data(), d_dsts, nq * 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    const uint32_t inf = EAT_INF;
-    for (uint64_t q = 0; q < nq; ++q) {
-        if (hs[q] >= h->hx.n || ht[q] >= EAT_INF || hd[q] >= h->hx.n) {
-            CUDA_TRY(cudaMemcpyAsync(d_out + q, &inf, 4, cudaMemcpyHostToDevice, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-            continue;
-        }
-        eat_status e = enqueue_single(h, hs[q], ht[q], h->d_out1, st);
-        if (e != EAT_OK) return e;
-        CUDA_TRY(cudaMemcpyAsync(d_out + q, h->d_out1 + hd[q], 4, cudaMemcpyDeviceToDevice, st));
-    }
-    return EAT_OK;
+    // e[] too large for shared memory: CTA groups, e[dst] of each query
+    return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, h->d_counter, d_dsts);
 }
 
 eat_status eat_query_many_target(eat_handle *h, const uint32_t *sources, const uint32_t *times, const uint32_t *dsts,

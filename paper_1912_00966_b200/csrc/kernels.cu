@@ -690,7 +690,8 @@ __device__ __forceinline__ void grid_solve(const DevIndex &ix, const GridWork &w
         ++sweep;
         if (cnt_cur == 0u) break;
     }
-    for (uint64_t i = gtid; i < n; i += gsz) out[i] = ld_cg(w.arr + __ldg(ix.perm + i));
+    if (out)  // caller-ordered row (NULL: the caller reads w.arr itself)
+        for (uint64_t i = gtid; i < n; i += gsz) out[i] = ld_cg(w.arr + __ldg(ix.perm + i));
     if (gtid == 0) w.ctl[8] = sweep;
 }
 
@@ -712,7 +713,8 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_groups(DevIndex ix, c
                                                                const uint32_t *__restrict__ tsv, uint64_t nq,
                                                                uint32_t *__restrict__ out,
                                                                unsigned long long *qcounter,
-                                                               unsigned long long *invalid) {
+                                                               unsigned long long *invalid,
+                                                               const uint32_t *__restrict__ dstv) {
     const uint32_t g = blockIdx.x / cpg, crank = blockIdx.x % cpg;
     const GridWork w = ws[g];
     const uint64_t gtid = crank * uint64_t(kGridThreads) + threadIdx.x, gsz = uint64_t(cpg) * kGridThreads;
@@ -725,14 +727,20 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_groups(DevIndex ix, c
         }
         const uint32_t q = grid_sync(bar, epoch, cpg, w.ctl + 20);  // also: the previous row is written
         if (q == 0xFFFFFFFFu) break;
-        uint32_t *orow = out + uint64_t(q) * ix.n;
-        const uint32_t s = src[q], ts = tsv[q];
-        if (s >= ix.n || ts >= kInf) {
-            for (uint64_t i = gtid; i < ix.n; i += gsz) orow[i] = kInf;
+        // goal-directed queries (dstv, NEXT-4): only e[dst] is written, out[q]
+        uint32_t *orow = dstv ? out + q : out + uint64_t(q) * ix.n;
+        const uint32_t s = src[q], ts = tsv[q], dq = dstv ? dstv[q] : 0u;
+        if (s >= ix.n || ts >= kInf || dq >= ix.n) {
+            if (dstv) {
+                if (gtid == 0) orow[0] = kInf;
+            } else {
+                for (uint64_t i = gtid; i < ix.n; i += gsz) orow[i] = kInf;
+            }
             if (gtid == 0) atomicAdd(invalid, 1ull);
             continue;
         }
-        grid_solve<SW, kSchedFrontier>(ix, w, s, ts, orow, gtid, gsz, cpg, bar, epoch);
+        grid_solve<SW, kSchedFrontier>(ix, w, s, ts, dstv ? nullptr : orow, gtid, gsz, cpg, bar, epoch);
+        if (dstv && gtid == 0) orow[0] = ld_cg(w.arr + __ldg(ix.perm + dq));
     }
 }
 
@@ -793,7 +801,8 @@ cudaError_t launch_cta_variant(const DevIndex &ix, const CtaArgs &a, cudaStream_
 template <int SW>
 cudaError_t launch_groups_sw(const DevIndex &ix, const GridWork *h_ws, const GridWork *d_ws, uint32_t groups,
                              const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
-                             unsigned long long *qcounter, unsigned long long *invalid, cudaStream_t st) {
+                             unsigned long long *qcounter, unsigned long long *invalid, const uint32_t *dst,
+                             cudaStream_t st) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -809,7 +818,7 @@ cudaError_t launch_groups_sw(const DevIndex &ix, const GridWork *h_ws, const Gri
     DevIndex ixc = ix;
     const GridWork *wp = d_ws;
     uint32_t c = cpg;
-    void *args[] = {&ixc, &wp, &c, &src, &ts, &nq, &out, &qcounter, &invalid};
+    void *args[] = {&ixc, &wp, &c, &src, &ts, &nq, &out, &qcounter, &invalid, &dst};
     return cudaLaunchCooperativeKernel((const void *)k_query_groups<SW>, dim3(groups * cpg), dim3(kGridThreads), args,
                                        0, st);
 }
@@ -895,15 +904,16 @@ cudaError_t launch_query_cta(const DevIndex &ix, const CtaArgs &a, cudaStream_t 
 
 cudaError_t launch_query_groups(const DevIndex &ix, int subwarp, const GridWork *h_ws, const GridWork *d_ws,
                                 uint32_t groups, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
-                                unsigned long long *qcounter, unsigned long long *invalid, cudaStream_t st) {
+                                unsigned long long *qcounter, unsigned long long *invalid, const uint32_t *dst,
+                                cudaStream_t st) {
     if (nq == 0) return cudaSuccess;
     switch (subwarp) {
-        case 1: return launch_groups_sw<1>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
-        case 2: return launch_groups_sw<2>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
-        case 4: return launch_groups_sw<4>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
-        case 8: return launch_groups_sw<8>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
-        case 16: return launch_groups_sw<16>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
-        default: return launch_groups_sw<32>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, st);
+        case 1: return launch_groups_sw<1>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
+        case 2: return launch_groups_sw<2>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
+        case 4: return launch_groups_sw<4>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
+        case 8: return launch_groups_sw<8>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
+        case 16: return launch_groups_sw<16>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
+        default: return launch_groups_sw<32>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
     }
 }
 

@@ -79,10 +79,12 @@ cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const 
 
 // Batched queries with e[] in global memory: `groups` CTA groups of one
 // cooperative launch, each with its own scratch (h_ws host copy / d_ws device
-// array of GridWork), solve the nq queries (frontier schedule); row q of out.
+// array of GridWork), solve the nq queries (frontier schedule); row q of out,
+// or out[q] = e[dst[q]] when dst != NULL (goal-directed).
 cudaError_t launch_query_groups(const DevIndex &ix, int subwarp, const GridWork *h_ws, const GridWork *d_ws,
                                 uint32_t groups, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
-                                unsigned long long *qcounter, unsigned long long *invalid, cudaStream_t st);
+                                unsigned long long *qcounter, unsigned long long *invalid, const uint32_t *dst,
+                                cudaStream_t st);
 
 // CTAs per SM of the persistent grid kernels (env EAT_GRID_CTAS_PER_SM, default 1).
 int grid_ctas_per_sm();

@@ -244,7 +244,13 @@ def test_metro_batched_groups():
     got = out.cpu().numpy().astype(np.uint32)
     assert (got[5] == INF).all()
     keep = np.arange(src.size) != 5
-    _assert_rows(got[keep], csa.query_many(src[keep], ts[keep]), "metro batch (device)")
+    want = csa.query_many(src[keep], ts[keep])
+    _assert_rows(got[keep], want, "metro batch (device)")
+    # goal-directed on the same path: e[dst] only
+    dst = (np.arange(src.size, dtype=np.int64) * 7919) % tt.num_vertices
+    tgt = eng.query_targets(src, ts, dst.astype(np.uint32))
+    full = csa.query_many(src, ts)
+    assert np.array_equal(tgt, full[np.arange(src.size), dst])
 
 
 # ----------------------------------------------------------------------------- edge partition

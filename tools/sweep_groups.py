@@ -14,7 +14,7 @@ want = {i: csa.query(int(src[i]), int(ts[i])) for i in range(0, nq, nq // 8)}
 d_src = torch.tensor(src.astype(np.int32), device="cuda")
 d_ts = torch.tensor(ts.astype(np.int32), device="cuda")
 out = torch.empty((nq, tt.num_vertices), dtype=torch.int32, device="cuda")
-for g in (1, 2, 4, 8, 16, 37, 74):
+for g in [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "1,2,4,8,16,37,74").split(",")]:
     os.environ["EAT_BATCH_GROUPS"] = str(g)
     eng = Engine.from_timetable(tt, subtrips=3)
     eng.query_many_device(d_src, d_ts, out)
