@@ -36,6 +36,12 @@ sys.path.insert(0, ROOT)
 METRIC = "EAT queries/s"
 UNIT = "queries/s"
 QUERIES_PER_RANK = (1000, 10)  # sources x times
+BATCH_WORKLOADS = {
+    # name: (synth config, (sources, times) per rank, description)
+    "city_batch": ("city", QUERIES_PER_RANK, "city_batch_10k (BASELINE configs[2]; 10k queries per GPU)"),
+    "metro_batch": ("metro", (256, 4), "metro_batch_1k (SURVEY 8(a) a12 with e[] in global memory: 1,024 "
+                                       "metro queries per GPU, CTA groups of one launch)"),
+}
 L2_READ_GBS = 17805.0  # measured L2-resident read bandwidth, 32 MiB working set (profiles/r01_ncu_summary.md)
 
 
@@ -165,7 +171,7 @@ def _cpu_baseline(tt, src, ts, budget_s: float):
     dt = time.perf_counter() - t0
     csa.close()
     return {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {done} of the {src.size} city-batch queries, serial CSA (oracle/csa.c, gcc -O3), "
+            "sample": f"first {done} of the {src.size} batch queries, serial CSA (oracle/csa.c, gcc -O3), "
                       f"{dt:.1f} s on 1 host core"}
 
 
@@ -319,6 +325,37 @@ def run_single(args):
         torch.distributed.destroy_process_group()
 
 
+def _batch_roofline(tt, src, ts, dev, args, step_ms, st0):
+    """roofline object of the batched kernel: algorithmic bytes (instrumented
+    CTA-kernel run on the same queries) / mean launch time vs the HBM peak."""
+    if st0["cta_grid"] == 0:  # grouped grid kernel: no instrumented variant for byte accounting
+        return {"bound": "hbm", "achieved": None, "peak": _peaks()[0], "unit": "GB/s", "frac": None, "traffic": None,
+                "kernel": "k_query_groups", "note": "latency-bound frontier sweeps (DESIGN.md §9)"}
+    try:
+        from paper_1912_00966_b200 import counters
+
+        cnt = counters.count_batch(tt, src, ts, dev, subtrips=args.subtrips)
+        alg_bytes = cnt["algorithmic_bytes"]
+        mean_launch_s = (sum(step_ms) / len(step_ms)) / 1e3
+        peak, peak_src = _peaks()
+        achieved = alg_bytes / mean_launch_s / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic_city_batch.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src, "kernel": "k_query_cta",
+                "algorithmic_bytes_per_launch": alg_bytes, "counters": cnt,
+                # the index is L2-resident: the same bytes against the measured
+                # L2-resident read bandwidth (tools/l2_bw.py, profiles/r01_ncu_summary.md)
+                "l2": {"peak": L2_READ_GBS, "frac": achieved / L2_READ_GBS,
+                       "note": "kernel is issue-bound (ncu: IPC 2.44 of 4), not bandwidth-bound"}}
+    except Exception as exc:  # keep the bench line even if accounting fails
+        return {"bound": "hbm", "achieved": None, "peak": _peaks()[0], "unit": "GB/s", "frac": None,
+                "traffic": None, "error": repr(exc)}
+
+
 def run_gpu(args):
     import torch
 
@@ -326,8 +363,9 @@ def run_gpu(args):
     import synth
     from paper_1912_00966_b200 import Engine
 
-    tt = synth.generate("city")
-    nsrc, ntime = QUERIES_PER_RANK
+    cfg_name, (nsrc, ntime), wl_desc = BATCH_WORKLOADS[args.workload]
+    city = cfg_name == "city"
+    tt = synth.generate(cfg_name)
     all_src, all_ts = synth.queries(tt, nsrc * world, ntime)
     per = nsrc * ntime
     src, ts = all_src[rank * per:(rank + 1) * per], all_ts[rank * per:(rank + 1) * per]
@@ -375,7 +413,7 @@ def run_gpu(args):
     # index) and the paper's scheme 2 (r = sqrt(average trip length))
     variants = {}
     for st_alt, key in ((0, "no_subtrips_queries_per_s_per_gpu"), (2, "paper_scheme2_queries_per_s_per_gpu")):
-        if st_alt == args.subtrips:
+        if st_alt == args.subtrips or not city:
             continue
         eng0 = Engine.from_timetable(tt, device=dev, kernel="auto", subtrips=st_alt)
         for _ in range(2):
@@ -420,7 +458,7 @@ def run_gpu(args):
     s1, t1 = synth.SINGLE_QUERY
     o1 = torch.empty(tt.num_vertices, dtype=torch.int32, device=dev)
     single = {}
-    for kname in ("cta", "frontier"):
+    for kname in (("cta", "frontier") if city else ()):
         e1 = Engine.from_timetable(tt, device=dev, kernel=kname, subtrips=args.subtrips)
         for _ in range(3):
             e1.query_device(s1, t1, o1, stream=stream)
@@ -436,30 +474,7 @@ def run_gpu(args):
         e1.close()
 
     # ---- algorithmic bytes of the batched kernel (counters from an instrumented run)
-    roof = None
-    try:
-        from paper_1912_00966_b200 import counters
-
-        cnt = counters.count_batch(tt, src, ts, dev, subtrips=args.subtrips)
-        alg_bytes = cnt["algorithmic_bytes"]
-        mean_launch_s = (sum(step_ms) / len(step_ms)) / 1e3
-        peak, peak_src = _peaks()
-        achieved = alg_bytes / mean_launch_s / 1e9
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic_city_batch.json")
-        if os.path.exists(tp):
-            with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src, "kernel": "k_query_cta",
-                "algorithmic_bytes_per_launch": alg_bytes, "counters": cnt,
-                # the index is L2-resident: the same bytes against the measured
-                # L2-resident read bandwidth (tools/l2_bw.py, profiles/r01_ncu_summary.md)
-                "l2": {"peak": L2_READ_GBS, "frac": achieved / L2_READ_GBS,
-                       "note": "kernel is issue-bound (ncu: IPC 2.44 of 4), not bandwidth-bound"}}
-    except Exception as exc:  # keep the bench line even if accounting fails
-        roof = {"bound": "hbm", "achieved": None, "peak": _peaks()[0], "unit": "GB/s", "frac": None,
-                "traffic": None, "error": repr(exc)}
+    roof = _batch_roofline(tt, src, ts, dev, args, step_ms, st0)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -471,18 +486,19 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": "city_batch_10k (BASELINE configs[2]; 10k queries per GPU)",
+            "config": {"workload": wl_desc,
                        "stops": tt.num_vertices, "edges": st0["num_edges"], "connections": tt.num_connections,
                        "types": st0["num_types"], "queries_per_gpu": nq, "parallelism": f"query-sharded x{world}",
                        "l2": "flushed (256 MiB write) between timed steps",
-                       "kernel": "cta (batched)" if st0["cta_grid"] > 0 else "per-query " + st0["kernel_name"],
-                       "subtrips": args.subtrips, "window_s": 1200, "cta_threads": 256,
+                       "kernel": "cta (batched)" if st0["cta_grid"] > 0 else "grid groups (k_query_groups, frontier)",
+                       "subtrips": args.subtrips, "window_s": 1200 if st0["cta_grid"] > 0 else None,
+                       "cta_threads": 256 if st0["cta_grid"] > 0 else None,
                        "shortcuts": st0["num_shortcuts"]},
             "connections_resolved_per_s": resolved / (tot_ms / 1e3),
             "variants": variants,
             "single_query_ms": {k: v["ms"] for k, v in single.items()},
             "single_query_sweeps": {k: v["sweeps"] for k, v in single.items()},
-            "single_query_config": "city, s=0, t_s=06:00 (BASELINE configs[1]), device time per query",
+            "single_query_config": "city, s=0, t_s=06:00 (BASELINE configs[1]), device time per query" if city else None,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(nq * 8),
                     "d2h_bytes_per_step": int(nq * tt.num_vertices * 4), "host_buffers": "pinned",
                     "rows_match_device_run": e2e_ok},
@@ -509,7 +525,7 @@ def main():
                     help="sub-trip shortcuts (PAPER.md:342-354): 0 off, 1 r=sqrt(k) per trip, 2 r=sqrt(avg) "
                          "(the paper's scheme 2), >=3 fixed r (default 3: +3 %% q/s over scheme 2 on B200, "
                          "profiles/r01_sweep_subtrips_r.jsonl)")
-    ap.add_argument("--workload", default="city_batch", choices=["city_batch"] + sorted(SINGLE_WORKLOADS))
+    ap.add_argument("--workload", default="city_batch", choices=sorted(BATCH_WORKLOADS) + sorted(SINGLE_WORKLOADS))
     ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "peer"],
                     help="country_part: per-round NCCL min-allreduce of e[] (BASELINE configs[4]) or the in-kernel "
                          "peer exchange over NVLink (NEXT-2, CUDA IPC between the ranks)")
@@ -518,7 +534,7 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload == "city_batch":
+    elif args.workload in BATCH_WORKLOADS:
         run_gpu(args)
     else:
         run_single(args)

@@ -108,6 +108,7 @@ struct eat_handle {
     uint32_t *d_bsrc[2] = {nullptr, nullptr}, *d_bts[2] = {nullptr, nullptr}, *d_bout[2] = {nullptr, nullptr};
     uint32_t *h_stage[2] = {nullptr, nullptr};
     unsigned long long *d_bcounter = nullptr;  // [2]
+    cudaEvent_t bev[4] = {nullptr, nullptr, nullptr, nullptr};  // chunk kernel done [0..1], rows copied [2..3]
     uint64_t bcap = 0, stage_cap = 0;
     // direct mode (pinned host output, CTA kernel): all queries in one launch,
     // rows stored by the kernel straight into the mapped host buffer
@@ -181,6 +182,8 @@ void release_device(eat_handle *h) {
         if (h->h_stage[i]) cudaFreeHost(h->h_stage[i]);
         if (h->bstream[i]) cudaStreamDestroy(h->bstream[i]);
     }
+    for (cudaEvent_t ev : h->bev)
+        if (ev) cudaEventDestroy(ev);
     if (h->comm) ncclCommDestroy(h->comm);
     for (void *p : h->peer_mapped)
         if (p) cudaIpcCloseMemHandle(p);
@@ -961,23 +964,33 @@ eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t
         for (int i = 0; i < 2; ++i) CUDA_TRY(cudaMallocHost(&h->h_stage[i], chunk * n * 4));
         h->stage_cap = chunk;
     }
+    // Kernels (and their inputs) in order on stream 0, row copies on stream 1:
+    // chunk i's copy overlaps chunk i+1's kernel; chunk i+2 reuses the buffers
+    // after chunk i's copy.  One compute stream keeps cooperative grid-group
+    // launches (graphs without shared-memory e[]) from running concurrently.
+    if (!h->bev[0])
+        for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreateWithFlags(&h->bev[i], cudaEventDisableTiming));
+    cudaStream_t cs = h->bstream[0], ks = h->bstream[1];
     const uint64_t nchunks = (nq + chunk - 1) / chunk;
     for (uint64_t i = 0; i <= nchunks; ++i) {
         if (i < nchunks) {
             const int b = int(i & 1);
             const uint64_t q0 = i * chunk, c = std::min(chunk, nq - q0);
-            cudaStream_t st = h->bstream[b];
-            CUDA_TRY(cudaMemcpyAsync(h->d_bsrc[b], sources + q0, c * 4, cudaMemcpyHostToDevice, st));
-            CUDA_TRY(cudaMemcpyAsync(h->d_bts[b], times + q0, c * 4, cudaMemcpyHostToDevice, st));
-            eat_status e = enqueue_batch(h, h->d_bsrc[b], h->d_bts[b], c, h->d_bout[b], st, h->d_bcounter + b, 1 + b);
+            if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(cs, h->bev[2 + b], 0));  // chunk i-2's rows copied out
+            CUDA_TRY(cudaMemcpyAsync(h->d_bsrc[b], sources + q0, c * 4, cudaMemcpyHostToDevice, cs));
+            CUDA_TRY(cudaMemcpyAsync(h->d_bts[b], times + q0, c * 4, cudaMemcpyHostToDevice, cs));
+            eat_status e = enqueue_batch(h, h->d_bsrc[b], h->d_bts[b], c, h->d_bout[b], cs, h->d_bcounter + b, 1 + b);
             if (e != EAT_OK) return e;
+            CUDA_TRY(cudaEventRecord(h->bev[b], cs));
+            CUDA_TRY(cudaStreamWaitEvent(ks, h->bev[b], 0));
             CUDA_TRY(cudaMemcpyAsync(pinned ? out + q0 * n : h->h_stage[b], h->d_bout[b], c * n * 4,
-                                     cudaMemcpyDeviceToHost, st));
+                                     cudaMemcpyDeviceToHost, ks));
+            CUDA_TRY(cudaEventRecord(h->bev[2 + b], ks));
         }
         if (i >= 1) {  // retire chunk i-1 (its stage is reused by chunk i+1)
             const int b = int((i - 1) & 1);
             const uint64_t q0 = (i - 1) * chunk, c = std::min(chunk, nq - q0);
-            CUDA_TRY(cudaStreamSynchronize(h->bstream[b]));
+            CUDA_TRY(cudaEventSynchronize(h->bev[2 + b]));
             if (!pinned) host_copy(out + q0 * n, h->h_stage[b], c * n * 4);
         }
     }

@@ -253,6 +253,25 @@ def test_metro_batched_groups():
     assert np.array_equal(tgt, full[np.arange(src.size), dst])
 
 
+@pytest.mark.timeout(600)
+def test_metro_batched_chunked_pipeline():
+    """eat_query_many with more queries than one pipeline chunk (640 metro
+    rows): chunk kernels share one compute stream (cooperative grid-group
+    launches must not overlap), row copies overlap on the copy stream;
+    pageable and page-locked outputs; sampled rows equal the oracle's."""
+    from paper_1912_00966_b200 import pinned_empty
+
+    tt = synth.generate("metro")
+    eng = Engine.from_timetable(tt, subtrips=3)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    src, ts = synth.queries(tt, 350, 4, seed=5)  # 1,400 queries: 3 chunks
+    pin = pinned_empty((src.size, tt.num_vertices))
+    for out in (None, pin):
+        got = eng.query_many(src, ts, out=out)
+        for i in list(range(0, src.size, 173)) + [src.size - 1]:
+            _assert_rows(got[i:i + 1], csa.query_many(src[i:i + 1], ts[i:i + 1]), f"metro chunked row {i}")
+
+
 # ----------------------------------------------------------------------------- edge partition
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
 def test_edge_partitioned_loopback(P):
