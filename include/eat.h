@@ -27,7 +27,10 @@
  *     ABI; on error outputs are left untouched (host variants) or unspecified
  *     (device variants) and eat_last_error() returns a thread-local message.
  *   - Threading: a handle is immutable after eat_build; calls on one handle
- *     are serialised by an internal mutex; distinct handles are independent.
+ *     are serialised by an internal mutex, and their device work too: a
+ *     *_device call's stream first waits for the previous call's work on the
+ *     handle (whatever its stream), host calls wait for it; distinct handles
+ *     are independent.
  *   - There is no CPU fallback: every query runs in the CUDA kernels of
  *     libeat.so; without a usable CUDA device the query calls return
  *     EAT_ECUDA.

@@ -109,6 +109,10 @@ struct eat_handle {
     uint32_t *h_stage[2] = {nullptr, nullptr};
     unsigned long long *d_bcounter = nullptr;  // [2]
     cudaEvent_t bev[4] = {nullptr, nullptr, nullptr, nullptr};  // chunk kernel done [0..1], rows copied [2..3]
+    // end of the last device work enqueued on this handle: the next call's
+    // stream waits for it (the handle's scratch is shared, and two cooperative
+    // grid kernels must never run concurrently)
+    cudaEvent_t order_ev = nullptr;
     uint64_t bcap = 0, stage_cap = 0;
     // direct mode (pinned host output, CTA kernel): all queries in one launch,
     // rows stored by the kernel straight into the mapped host buffer
@@ -184,6 +188,7 @@ void release_device(eat_handle *h) {
     }
     for (cudaEvent_t ev : h->bev)
         if (ev) cudaEventDestroy(ev);
+    if (h->order_ev) cudaEventDestroy(h->order_ev);
     if (h->comm) ncclCommDestroy(h->comm);
     for (void *p : h->peer_mapped)
         if (p) cudaIpcCloseMemHandle(p);
@@ -499,6 +504,18 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
     return EAT_OK;
 }
 
+// Orders device work of successive calls on one handle across streams:
+// the call's stream waits for the previous call's work, then records its own.
+struct HandleOrder {
+    eat_handle *h;
+    cudaStream_t st;
+    HandleOrder(eat_handle *h_, cudaStream_t st_) : h(h_), st(st_) {
+        if (!h->order_ev) cudaEventCreateWithFlags(&h->order_ev, cudaEventDisableTiming);
+        cudaStreamWaitEvent(st, h->order_ev, 0);
+    }
+    ~HandleOrder() { cudaEventRecord(h->order_ev, st); }
+};
+
 }  // namespace
 
 extern "C" {
@@ -711,6 +728,7 @@ eat_status eat_query_device(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_TRY(cudaSetDevice(h->device));
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    HandleOrder order(h, st);
     if (h->mode == EAT_MODE_EDGE_PARTITIONED) return run_partitioned(h, s, t_s, d_out, st);
     return enqueue_single(h, s, t_s, d_out, st);
 }
@@ -721,6 +739,7 @@ eat_status eat_query(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *out_arr)
     if (!out_arr) return fail(EAT_EINVAL, "NULL output");
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_TRY(cudaSetDevice(h->device));
+    if (h->order_ev) CUDA_TRY(cudaEventSynchronize(h->order_ev));  // device calls still in flight
     if (h->mode == EAT_MODE_EDGE_PARTITIONED) {
         e = run_partitioned(h, s, t_s, h->d_out1, h->stream);
         if (e != EAT_OK) return e;
@@ -838,7 +857,9 @@ eat_status eat_query_many_device(eat_handle *h, const uint32_t *d_sources, const
         return fail(EAT_ESTATE, "batched queries need a replicated handle (query-parallel sharding)");
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_TRY(cudaSetDevice(h->device));
-    return enqueue_batch(h, d_sources, d_times, nq, d_out, static_cast<cudaStream_t>(cuda_stream), h->d_counter);
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    HandleOrder order(h, st);
+    return enqueue_batch(h, d_sources, d_times, nq, d_out, st, h->d_counter);
 }
 
 eat_status eat_query_many_target_device(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times,
@@ -852,6 +873,7 @@ eat_status eat_query_many_target_device(eat_handle *h, const uint32_t *d_sources
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_TRY(cudaSetDevice(h->device));
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    HandleOrder order(h, st);
     if (h->cta_grid > 0) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, h->d_counter, 0, d_dsts);
     // e[] too large for shared memory: CTA groups, e[dst] of each query
     return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, h->d_counter, d_dsts);
@@ -872,6 +894,7 @@ eat_status eat_query_many_target(eat_handle *h, const uint32_t *sources, const u
     {
         std::lock_guard<std::mutex> lk(h->mu);
         CUDA_TRY(cudaSetDevice(h->device));
+    if (h->order_ev) CUDA_TRY(cudaEventSynchronize(h->order_ev));  // device calls still in flight
         CUDA_TRY(cudaMallocAsync(&d, nq * 16, h->stream));
         CUDA_TRY(cudaMemcpyAsync(d, sources, nq * 4, cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(cudaMemcpyAsync(d + nq, times, nq * 4, cudaMemcpyHostToDevice, h->stream));
@@ -901,6 +924,7 @@ eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t
     }
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_TRY(cudaSetDevice(h->device));
+    if (h->order_ev) CUDA_TRY(cudaEventSynchronize(h->order_ev));  // device calls still in flight
     const uint64_t n = h->hx.n;
     // Two-stage pipeline over chunks of queries (stream i&1): H2D queries ->
     // batched kernel -> D2H rows, so chunk i+1 computes while chunk i copies.

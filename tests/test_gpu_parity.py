@@ -272,6 +272,32 @@ def test_metro_batched_chunked_pipeline():
             _assert_rows(got[i:i + 1], csa.query_many(src[i:i + 1], ts[i:i + 1]), f"metro chunked row {i}")
 
 
+def test_device_calls_on_two_streams_are_ordered():
+    """Device calls on one handle from different streams (no user sync in
+    between) run one after another: rows stay exact, and cooperative grid
+    kernels never overlap (they would deadlock)."""
+    import torch
+
+    tt = synth.generate("metro")
+    eng = Engine.from_timetable(tt, subtrips=3)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    qs = [synth.SINGLE_QUERY, (4242, 40000), (99, 70000)]
+    outs = [torch.empty(tt.num_vertices, dtype=torch.int32, device="cuda") for _ in qs]
+    src, ts = synth.queries(tt, 4, 2, seed=9)
+    d_src = torch.tensor(src.astype(np.int32), device="cuda")
+    d_ts = torch.tensor(ts.astype(np.int32), device="cuda")
+    rows = torch.empty((src.size, tt.num_vertices), dtype=torch.int32, device="cuda")
+    for k, (q, o) in enumerate(zip(qs, outs)):
+        eng.query_device(*q, o, stream=s1 if k % 2 == 0 else s2)
+        if k == 1:
+            eng.query_many_device(d_src, d_ts, rows, stream=s1)
+    torch.cuda.synchronize()
+    for q, o in zip(qs, outs):
+        _assert_rows(o.cpu().numpy().astype(np.uint32)[None], csa.query(*q)[None], f"two streams {q}")
+    _assert_rows(rows.cpu().numpy().astype(np.uint32), csa.query_many(src, ts), "two streams batch")
+
+
 # ----------------------------------------------------------------------------- edge partition
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
 def test_edge_partitioned_loopback(P):
