@@ -410,11 +410,11 @@ eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_
 }
 
 // CTA groups (queries in flight) of the batched kernel when e[] does not fit
-// shared memory: nq / 4, at most 74 (two CTAs per group); metro 256 queries
-// 1.1k q/s with one group -> 11.2k q/s with 74, country 64 queries best at 16
-// (tools/sweep_groups.py, profiles/r01_sweep_batch_groups.jsonl).
+// shared memory: nq / 8, at most 296 (two 512-thread CTAs per group); metro
+// 2,048 queries 19.8k q/s at 148-592 groups, country 512 queries best at 64
+// (tools/sweep_groups.py, profiles/r01_sweep_group_shape.jsonl).
 // EAT_BATCH_GROUPS overrides.
-constexpr uint32_t kBatchGroupsMax = 74;
+constexpr uint32_t kBatchGroupsMax = 296;
 
 // Largest graph whose single queries AUTO runs on the one-CTA kernel.
 constexpr uint32_t kAutoCtaMaxVertices = 2048;
@@ -803,8 +803,10 @@ eat_status launch_batch_cta(eat_handle *h, const uint32_t *d_sources, const uint
 // goal-directed, out[q] = e[dst[q]].
 eat_status launch_batch_groups(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
                                uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, const uint32_t *d_dst) {
-    uint32_t groups = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(kBatchGroupsMax, nq / 4)));
-    if (const char *gv = getenv("EAT_BATCH_GROUPS")) groups = uint32_t(std::max(1, std::min(148, atoi(gv))));
+    uint32_t groups = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(kBatchGroupsMax, nq / 8)));
+    // scratch is ~32 B per vertex per group: keep it under 4 GB
+    groups = uint32_t(std::min<uint64_t>(groups, std::max<uint64_t>(1, (4ull << 30) / (32ull * h->hx.n + 1))));
+    if (const char *gv = getenv("EAT_BATCH_GROUPS")) groups = uint32_t(std::max(1, std::min(592, atoi(gv))));
     groups = uint32_t(std::min<uint64_t>(groups, nq));
     if (h->bgw.size() < groups) {
         CUDA_TRY(cudaStreamSynchronize(st));

@@ -707,8 +707,14 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_grid(DevIndex ix, Gri
 // in global memory): the grid splits into groups of cpg CTAs; each group
 // takes queries from a global counter and solves them one after another
 // with the frontier schedule, using its own scratch (ws[g]) and barrier.
+// 512-thread CTAs, four per SM (32 registers): 64 warps per SM hide the
+// latency of many concurrent queries (metro batch 12.8k -> 18.8k q/s vs one
+// 1024-thread CTA per SM, profiles/r01_sweep_group_shape.jsonl).
+constexpr int kGroupThreads = 512;
+constexpr int kGroupMinBlocks = 4;
+
 template <int SW>
-__global__ void __launch_bounds__(kGridThreads, 1) k_query_groups(DevIndex ix, const GridWork *__restrict__ ws,
+__global__ void __launch_bounds__(kGroupThreads, kGroupMinBlocks) k_query_groups(DevIndex ix, const GridWork *__restrict__ ws,
                                                                uint32_t cpg, const uint32_t *__restrict__ src,
                                                                const uint32_t *__restrict__ tsv, uint64_t nq,
                                                                uint32_t *__restrict__ out,
@@ -717,7 +723,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) k_query_groups(DevIndex ix, c
                                                                const uint32_t *__restrict__ dstv) {
     const uint32_t g = blockIdx.x / cpg, crank = blockIdx.x % cpg;
     const GridWork w = ws[g];
-    const uint64_t gtid = crank * uint64_t(kGridThreads) + threadIdx.x, gsz = uint64_t(cpg) * kGridThreads;
+    const uint64_t gtid = crank * uint64_t(kGroupThreads) + threadIdx.x, gsz = uint64_t(cpg) * kGroupThreads;
     uint32_t *bar = w.ctl + kBarWord;
     uint32_t epoch = 0;
     for (;;) {
@@ -806,10 +812,9 @@ cudaError_t launch_groups_sw(const DevIndex &ix, const GridWork *h_ws, const Gri
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_groups<SW>, kGridThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_groups<SW>, kGroupThreads, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    per_sm = std::min(per_sm, grid_ctas_per_sm());
     const uint32_t cpg = uint32_t(sms * per_sm) / groups;
     if (cpg < 1) return cudaErrorInvalidConfiguration;
     for (uint32_t g = 0; g < groups; ++g)
@@ -819,7 +824,7 @@ cudaError_t launch_groups_sw(const DevIndex &ix, const GridWork *h_ws, const Gri
     const GridWork *wp = d_ws;
     uint32_t c = cpg;
     void *args[] = {&ixc, &wp, &c, &src, &ts, &nq, &out, &qcounter, &invalid, &dst};
-    return cudaLaunchCooperativeKernel((const void *)k_query_groups<SW>, dim3(groups * cpg), dim3(kGridThreads), args,
+    return cudaLaunchCooperativeKernel((const void *)k_query_groups<SW>, dim3(groups * cpg), dim3(kGroupThreads), args,
                                        0, st);
 }
 

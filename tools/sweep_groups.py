@@ -4,6 +4,9 @@ of sampled rows against the oracle.  Usage: python tools/sweep_groups.py [config
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth, oracle
+from paper_1912_00966_b200 import _lib
+if os.environ.get("EAT_AB_LIB"):
+    _lib.LIB_PATH = os.path.abspath(os.environ["EAT_AB_LIB"])
 from paper_1912_00966_b200 import Engine
 cfg = sys.argv[1] if len(sys.argv) > 1 else "metro"
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 256
@@ -23,5 +26,5 @@ for g in [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "1,2,4,8,16,37,
     a.record(); eng.query_many_device(d_src, d_ts, out); b.record(); b.synchronize()
     ms = a.elapsed_time(b)
     ok = all(np.array_equal(out[i].cpu().numpy().astype(np.uint32), w) for i, w in want.items())
-    print(json.dumps({"config": cfg, "groups": g, "queries": nq, "ms": ms, "qps": nq / ms * 1e3, "parity_sampled": ok}), flush=True)
+    print(json.dumps({"lib": os.path.basename(os.environ.get("EAT_AB_LIB", "libeat.so")), "config": cfg, "groups": g, "queries": nq, "ms": ms, "qps": nq / ms * 1e3, "parity_sampled": ok}), flush=True)
     eng.close()
