@@ -935,11 +935,11 @@ eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t
     cudaPointerAttributes pa{};
     const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    if (pinned && pa.devicePointer && h->cta_grid > 0 && h->e2e_direct) {
-        // Direct: one persistent launch over all queries; each CTA stores its
-        // finished rows into the page-locked host buffer over PCIe (mapped
-        // pointer), so the D2H traffic overlaps the relaxation of the other
-        // queries with no chunk head/tail.
+    if (pinned && pa.devicePointer && h->e2e_direct) {
+        // Direct: one persistent launch over all queries; each CTA (or CTA
+        // group) stores its finished rows into the page-locked host buffer
+        // over PCIe (mapped pointer), so the D2H traffic overlaps the
+        // relaxation of the other queries with no chunk head/tail.
         if (!h->bstream[0])
             for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&h->bstream[i], cudaStreamNonBlocking));
         if (!h->d_bcounter) CUDA_TRY(cudaMalloc(&h->d_bcounter, 2 * sizeof(unsigned long long)));

@@ -690,8 +690,18 @@ __device__ __forceinline__ void grid_solve(const DevIndex &ix, const GridWork &w
         ++sweep;
         if (cnt_cur == 0u) break;
     }
-    if (out)  // caller-ordered row (NULL: the caller reads w.arr itself)
+    // caller-ordered row (NULL: the caller reads w.arr itself); 16-byte
+    // stores when aligned (rows may live in mapped host memory)
+    if (out && (n & 3u) == 0u && (reinterpret_cast<uintptr_t>(out) & 15u) == 0u) {
+        const uint4 *pv = reinterpret_cast<const uint4 *>(ix.perm);
+        uint4 *ov = reinterpret_cast<uint4 *>(out);
+        for (uint64_t i = gtid; i < n / 4u; i += gsz) {
+            const uint4 pi = __ldg(pv + i);
+            ov[i] = make_uint4(ld_cg(w.arr + pi.x), ld_cg(w.arr + pi.y), ld_cg(w.arr + pi.z), ld_cg(w.arr + pi.w));
+        }
+    } else if (out) {
         for (uint64_t i = gtid; i < n; i += gsz) out[i] = ld_cg(w.arr + __ldg(ix.perm + i));
+    }
     if (gtid == 0) w.ctl[8] = sweep;
 }
 
