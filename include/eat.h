@@ -86,7 +86,8 @@ enum {
 /* eat_build_opts.kernel: relaxation schedule for single queries. */
 enum {
     EAT_KERNEL_AUTO = 0,          /* single queries: CTA kernel for graphs of <= 2048 stops, else FRONTIER; batches: CTA when e[] fits shared memory */
-    EAT_KERNEL_FRONTIER = 1,      /* grid-wide persistent kernel, worklist frontier, global arr */
+    EAT_KERNEL_FRONTIER = 1,      /* grid-wide persistent kernel, worklist frontier, global arr; requested
+                                     explicitly, batches also run this schedule (CTA groups, e[] in global) */
     EAT_KERNEL_FULL_SWEEP = 2,    /* grid-wide persistent kernel, every type every sweep, active bitmap */
     EAT_KERNEL_CTA = 3,           /* one CTA per query, arr in shared memory */
     EAT_KERNEL_ASYNC = 4,         /* CTA-partitioned: each CTA owns a vertex range (e[] slice in shared

@@ -120,6 +120,7 @@ struct eat_handle {
     uint64_t dcap = 0;
     bool e2e_direct = true;
     int cta_grid = 0;
+    bool batch_groups = false;  // batches on k_query_groups even when e[] fits shared memory (kernel FRONTIER)
     // edge partition
     uint32_t part_rank = 0, part_count = 1, part_lo = 0, part_hi = 0;
     ncclComm_t comm = nullptr;
@@ -436,6 +437,8 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     // when e[] fits (throughput).
     if (k == EAT_KERNEL_AUTO)
         k = (h->cta_grid > 0 && h->hx.n <= kAutoCtaMaxVertices) ? EAT_KERNEL_CTA : EAT_KERNEL_FRONTIER;
+    else if (k == EAT_KERNEL_FRONTIER)
+        h->batch_groups = true;  // explicit FRONTIER: batches use its schedule too (grouped grid kernel)
     if (k == EAT_KERNEL_CTA && h->cta_grid == 0)
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
     if (k == EAT_KERNEL_ASYNC && !async_ok)
@@ -826,7 +829,7 @@ eat_status launch_batch_groups(eat_handle *h, const uint32_t *d_sources, const u
 
 eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
                          uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, int slot = 0) {
-    if (h->cta_grid > 0) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, d_qcounter, slot, nullptr);
+    if (h->cta_grid > 0 && !h->batch_groups) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, d_qcounter, slot, nullptr);
     return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, d_qcounter, nullptr);
 }
 
@@ -876,7 +879,7 @@ eat_status eat_query_many_target_device(eat_handle *h, const uint32_t *d_sources
     CUDA_TRY(cudaSetDevice(h->device));
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     HandleOrder order(h, st);
-    if (h->cta_grid > 0) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, h->d_counter, 0, d_dsts);
+    if (h->cta_grid > 0 && !h->batch_groups) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, h->d_counter, 0, d_dsts);
     // e[] too large for shared memory: CTA groups, e[dst] of each query
     return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, h->d_counter, d_dsts);
 }

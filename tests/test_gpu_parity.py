@@ -298,6 +298,35 @@ def test_device_calls_on_two_streams_are_ordered():
     _assert_rows(rows.cpu().numpy().astype(np.uint32), csa.query_many(src, ts), "two streams batch")
 
 
+def test_grouped_batches_random_small():
+    """k_query_groups on adversarial small instances (explicit FRONTIER kernel
+    routes batches to the grouped grid kernel even when e[] fits shared
+    memory): every row equals the oracle's, invalid rows are INF."""
+    import torch
+
+    for seed in range(120):
+        tt = synth.random_small(9000 + seed)
+        eng = Engine.from_timetable(tt, kernel="frontier", subwarp=[32, 16, 8, 1][seed % 4],
+                                    continuation=[None, 0, 2][seed % 3])
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        rng = np.random.default_rng(seed)
+        nq = int(rng.integers(1, 70))
+        src = rng.integers(0, tt.num_vertices, nq).astype(np.uint32)
+        ts = rng.integers(0, 2 * 86400, nq).astype(np.uint32)
+        _assert_rows(eng.query_many(src, ts), csa.query_many(src, ts), f"groups seed {seed}")
+        if seed % 10 == 0:  # device path with an invalid query
+            bad = src.astype(np.int64)
+            bad[0] = tt.num_vertices
+            out = torch.empty((nq, tt.num_vertices), dtype=torch.int32, device="cuda")
+            eng.query_many_device(torch.tensor(bad.astype(np.int32), device="cuda"),
+                                  torch.tensor(ts.astype(np.int32), device="cuda"), out)
+            got = out.cpu().numpy().astype(np.uint32)
+            assert (got[0] == INF).all()
+            if nq > 1:
+                _assert_rows(got[1:], csa.query_many(src[1:], ts[1:]), f"groups device seed {seed}")
+        eng.close()
+
+
 # ----------------------------------------------------------------------------- edge partition
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
 def test_edge_partitioned_loopback(P):
