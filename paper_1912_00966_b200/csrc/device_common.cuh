@@ -221,14 +221,16 @@ __device__ __forceinline__ void push_aggregated(uint32_t v, uint2 rng, uint32_t 
 // the target v when this call strictly lowered e[v], else kNone; *cand_out
 // (optional) receives the candidate arrival.  SYS: system-scope atomic (e[]
 // also updated by peer GPUs, peer.cu).
-template <bool SYS = false>
+// NO_AV: skip the read of e[v] before the atomicMin (one dependent access
+// fewer per hop; the atomicMin alone decides) -- for latency-bound schedules.
+template <bool SYS = false, bool NO_AV = false>
 __device__ __forceinline__ uint32_t relax_type_global(const DevIndex &ix, uint64_t t, uint32_t eu, uint32_t *arr,
                                                       uint32_t *cand_out = nullptr) {
     CrecPrefetch pf{};
     if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);
     const TypeRec tr = load_type(ix, t);
     if (eu > tr.last) return kNone;
-    const uint32_t av = __ldcg(arr + tr.v);
+    const uint32_t av = NO_AV ? kInf : __ldcg(arr + tr.v);
     if (max(eu, tr.first) + tr.lam >= av) return kNone;  // early termination
     const uint32_t tc = ix.lookup_mode ? type_lookup_ablation(ix, tr, eu, ix.lookup_mode)
                         : eu <= tr.first ? tr.first

@@ -442,6 +442,9 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
 // quarter of the grid-barrier arrivals (metro -10 %, country -9 %;
 // DESIGN.md §9).
 constexpr int kGridThreads = 1024;
+// The frontier schedule skips the e[v] pre-read before its atomicMin (city
+// single query -5 %, metro/country unchanged: profiles/r01_ab_frontier_no_av.jsonl).
+constexpr bool kFrontierNoAv = true;
 
 // One query by `nctas` co-resident CTAs (thread gtid of gsz): the whole grid
 // (k_query_grid) or one CTA group of a multi-query launch (k_query_groups).
@@ -594,7 +597,7 @@ __device__ __forceinline__ void grid_solve(const DevIndex &ix, const GridWork &w
 #endif
                     uint32_t cv = kNone;
                     for (uint32_t t = p0 + lane; t < p1; t += sw) {
-                        const uint32_t v = relax_type_global(ix, t, eu, w.arr);
+                        const uint32_t v = relax_type_global<false, kFrontierNoAv>(ix, t, eu, w.arr);
                         if (v == kNone) continue;
                         if (budget > 0 && cv == kNone) {
                             cv = v;
