@@ -12,6 +12,12 @@
 //   - Relax (Algorithm 3) as atomicMin on e[v]
 //     (PAPER.md:403-409); a strict improvement marks v in the NEXT frontier.
 // Sweeps repeat until the next frontier is empty.
+//
+// Kernels: k_query_cta (one query per CTA, e[] in shared memory: batches and
+// small single queries), k_query_grid (one query on the whole GPU: frontier,
+// full-sweep, bitmap, connection and flattened schedules), k_query_groups
+// (batches whose e[] needs global memory: CTA groups, frontier schedule),
+// k_lookup (the lookup alone, for parity).
 #include <algorithm>
 #include <cstdlib>
 #include <cuda/atomic>
