@@ -52,7 +52,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "eat.h"))
     objs = []
-    for src in SOURCES:
+    procs = []
+    for src in SOURCES:  # translation units compile in parallel
         path = os.path.join(CSRC, src)
         obj = os.path.join(BUILD, src + ".o")
         objs.append(obj)
@@ -66,7 +67,15 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
             cmd += ["-Xptxas", "-v"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+        procs.append((subprocess.Popen(cmd), cmd, obj))
+    failed = None
+    for p, cmd, obj in procs:
+        if p.wait() != 0:
+            failed = failed or subprocess.CalledProcessError(p.returncode, cmd)
+            if os.path.exists(obj):
+                os.remove(obj)  # never link a stale object
+    if failed:
+        raise failed
     if force or _stale(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
         cmd = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-L", libdir, "-l:libnccl.so.2",
