@@ -144,9 +144,10 @@ typedef struct eat_build_opts {
                                      2 = r = round(sqrt(average trip length)); >= 3: r itself;
                                      EAT_SUBTRIPS_HIER + r (r >= 2): blocks of r, r^2, ... (ours).
                                      Arrival times are unchanged; sweeps (hops) drop. */
-    uint32_t arr_bits;            /* batched CTA kernel e[] in shared memory: 0/16 -> uint16 offsets from t_s
-                                     (twice the queries per SM; a query whose arrivals pass t_s + 65534 s is
-                                     recomputed with uint32), 32 -> uint32 only.  Results identical. */
+    uint32_t arr_bits;            /* batched CTA kernel e[] in shared memory: 0 or 32 -> uint32 (default);
+                                     16 -> uint16 offsets from t_s (twice the queries per SM; a query whose
+                                     arrivals pass t_s + 65534 s is recomputed with uint32; measured slower on
+                                     the city batch).  Results identical. */
     uint32_t lookup;              /* grid kernels, ablation (NEXT-3): 0 Cluster-AP;
                                      1 Connection-type-AP, Algorithm 6 over all AP tuples;
                                      2 Connection-type, linear getConnection */

@@ -29,7 +29,7 @@ EAT_BUILD_MULTIPROCESS = 0x4
 EAT_EXCHANGE = {"allreduce": 0, "peer": 1}
 EAT_PEER_HANDLE_BYTES = 64
 
-# symbols include/eat.h declares (checked by tests/test_abi.py)
+# symbols include/eat.h declares (checked by tests/test_index_host.py::test_abi_symbols_exported)
 EXPORTED = ["eat_build", "eat_query", "eat_query_device", "eat_query_many", "eat_query_many_device",
             "eat_query_many_target", "eat_query_many_target_device",
             "eat_lookup_device", "eat_get_stats", "eat_index_export", "eat_index_sizes", "eat_partition_range", "eat_peer_export", "eat_peer_connect", "eat_free", "eat_last_error",

@@ -120,6 +120,7 @@ struct eat_handle {
     uint64_t dcap = 0;
     bool e2e_direct = true;
     int cta_grid = 0;
+    uint32_t single_cta_threads = 1024;  // CTA variant of a lone query: 1024 when it fits, else cta_threads
     bool batch_groups = false;  // batches on k_query_groups even when e[] fits shared memory (kernel FRONTIER)
     // edge partition
     uint32_t part_rank = 0, part_count = 1, part_lo = 0, part_hi = 0;
@@ -422,6 +423,9 @@ constexpr uint32_t kAutoCtaMaxVertices = 2048;
 
 eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     h->cta_grid = eat::cta_grid_size(h->hx.n, int(h->cta_threads), h->arr16);
+    // a lone query takes the widest CTA (1024 threads, uint32 e[]) when its
+    // larger static shared memory still fits beside e[]; else the batch variant
+    h->single_cta_threads = eat::cta_grid_size(h->hx.n, 1024, false) > 0 ? 1024u : h->cta_threads;
     h->st.smem_vertices_max = 0;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
@@ -439,7 +443,7 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
         k = (h->cta_grid > 0 && h->hx.n <= kAutoCtaMaxVertices) ? EAT_KERNEL_CTA : EAT_KERNEL_FRONTIER;
     else if (k == EAT_KERNEL_FRONTIER)
         h->batch_groups = true;  // explicit FRONTIER: batches use its schedule too (grouped grid kernel)
-    if (k == EAT_KERNEL_CTA && h->cta_grid == 0)
+    if (k == EAT_KERNEL_CTA && (h->cta_grid == 0 || eat::cta_grid_size(h->hx.n, int(h->single_cta_threads), false) == 0))
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
     if (k == EAT_KERNEL_ASYNC && !async_ok)
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_ASYNC: a 1/SM-count slice of the arrival array does not fit shared memory");
@@ -488,7 +492,7 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
         a.sweeps = h->d_sweeps1;
         a.qcounter = h->d_counter;
         a.invalid = h->d_invalid;
-        a.threads = 1024;
+        a.threads = int(h->single_cta_threads);
         a.arr16 = false;
         a.grid_cap = 1;
         CUDA_TRY(eat::launch_query_cta(h->ix, a, st));

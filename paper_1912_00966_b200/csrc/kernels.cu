@@ -745,12 +745,17 @@ __global__ void __launch_bounds__(kGroupThreads, kGroupMinBlocks) k_query_groups
     const uint64_t gtid = crank * uint64_t(kGroupThreads) + threadIdx.x, gsz = uint64_t(cpg) * kGroupThreads;
     uint32_t *bar = w.ctl + kBarWord;
     uint32_t epoch = 0;
-    for (;;) {
+    // The query index is broadcast through ctl[20 + (iteration & 1)]: a slot
+    // is rewritten two iterations later, i.e. only after every CTA of the
+    // group passed the next iteration's barrier and so read it -- also when
+    // an invalid query skips grid_solve (and its barriers) entirely.
+    for (uint32_t iter = 0;; ++iter) {
+        uint32_t *slot = w.ctl + 20 + (iter & 1u);
         if (gtid == 0) {
             const unsigned long long qi = atomicAdd(qcounter, 1ull);
-            w.ctl[20] = qi < nq ? uint32_t(qi) : 0xFFFFFFFFu;
+            *slot = qi < nq ? uint32_t(qi) : 0xFFFFFFFFu;
         }
-        const uint32_t q = grid_sync(bar, epoch, cpg, w.ctl + 20);  // also: the previous row is written
+        const uint32_t q = grid_sync(bar, epoch, cpg, slot);  // also: the previous row is written
         if (q == 0xFFFFFFFFu) break;
         // goal-directed queries (dstv, NEXT-4): only e[dst] is written, out[q]
         uint32_t *orow = dstv ? out + q : out + uint64_t(q) * ix.n;

@@ -84,6 +84,11 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_query(const DevIndex *__r
     const bool leader = crank == 0;
     const uint32_t rbase = ld_cg(loc.ctl + 10);  // absolute round of this query's round 0 (slots, parity)
 
+    // The previous query's k_peer_gather on another rank may still read this
+    // block's e[] through its IPC mapping: no partition re-initializes before
+    // every partition has entered this query (its gather is stream-ordered
+    // before this launch).
+    peer_sync(lbar, lep, cpg, ctx.gctl, ctx.P, leader);
     // ---- Initialize (Algorithm 2): every replica, flags, frontier
     for (uint64_t i = gtid; i < n; i += gsz) {
         me.arr[i] = kInf;

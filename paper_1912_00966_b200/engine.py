@@ -31,6 +31,24 @@ def _stream_ptr(stream) -> int:
     return int(s.cuda_stream)
 
 
+def _check_tensor(t, numel: int, name: str, device: int) -> None:
+    """The C ABI cannot check device buffers: refuse a tensor that is not a
+    contiguous 4-byte CUDA tensor of exactly `numel` elements on `device`
+    (else the kernels would read or write past its end)."""
+    import torch
+
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch CUDA tensor")
+    if not t.is_cuda or (device >= 0 and t.device.index != device):
+        raise ValueError(f"{name} must live on cuda:{device} (got {t.device})")
+    if t.element_size() != 4 or t.dtype.is_floating_point:
+        raise ValueError(f"{name} must be int32/uint32 (got {t.dtype})")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements (got {t.numel()})")
+
+
 def pinned_empty(shape, dtype=np.uint32) -> np.ndarray:
     """Page-locked host array (torch pinned storage viewed as NumPy)."""
     import torch
@@ -79,6 +97,11 @@ class Engine:
                                    continuation=0 if continuation is None else (int(continuation) or _lib.EAT_CONT_NONE),
                                    exchange=_lib.EAT_EXCHANGE[exchange])
         self._h = _lib.eat_build(tt, opts)
+        self.device = -1 if host_only else int(device)
+        if self.device < 0 and not host_only:
+            import torch
+
+            self.device = torch.cuda.current_device()
         self.num_vertices = int(num_vertices)
         self.num_connections = int(m)
 
@@ -145,23 +168,32 @@ class Engine:
 
     def query_targets_device(self, sources, times, dsts, out, stream=None):
         """int32 CUDA tensors [nq]; out [nq] receives the arrival at each target."""
+        nq = int(sources.numel())
+        for t, nm in ((sources, "sources"), (times, "times"), (dsts, "dsts"), (out, "out")):
+            _check_tensor(t, nq, nm, self.device)
         _lib.eat_query_many_target_device(self._h, sources.data_ptr(), times.data_ptr(), dsts.data_ptr(),
                                           int(sources.numel()), out.data_ptr(), _stream_ptr(stream))
         return out
 
     def query_device(self, s: int, t_s: int, out, stream=None):
         """out: int32/uint32 CUDA tensor [num_vertices] on this engine's device."""
+        _check_tensor(out, self.num_vertices, "out", self.device)
         _lib.eat_query_device(self._h, int(s), int(t_s), out.data_ptr(), _stream_ptr(stream))
         return out
 
     def query_many_device(self, sources, times, out, stream=None):
         """sources, times: int32 CUDA tensors [nq]; out: int32 CUDA tensor [nq, num_vertices]."""
         nq = int(sources.numel())
+        _check_tensor(sources, nq, "sources", self.device)
+        _check_tensor(times, nq, "times", self.device)
+        _check_tensor(out, nq * self.num_vertices, "out", self.device)
         _lib.eat_query_many_device(self._h, sources.data_ptr(), times.data_ptr(), nq, out.data_ptr(),
                                    _stream_ptr(stream))
         return out
 
     def lookup_device(self, types, bounds, out, stream=None):
+        for t, nm in ((types, "types"), (bounds, "bounds"), (out, "out")):
+            _check_tensor(t, int(types.numel()), nm, self.device)
         _lib.eat_lookup_device(self._h, types.data_ptr(), bounds.data_ptr(), int(types.numel()), out.data_ptr(),
                                _stream_ptr(stream))
         return out

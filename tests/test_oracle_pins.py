@@ -207,6 +207,44 @@ def test_invariants_witness_and_monotone():
         c.close()
 
 
+def test_witness_ok_rejects_bad_witnesses():
+    """Negative pins for oracle.witness_ok: a valid
+    parent chain passes; each way a chain can fail to be a time-respecting
+    path ending exactly at e[x] is rejected."""
+    #            u  v  dep  dur
+    conns = [(0, 1, 100, 10),    # 0: e[1] = 110
+             (1, 2, 120, 10),    # 1: e[2] = 130
+             (2, 3, 140, 10),    # 2: e[3] = 150
+             (1, 2, 105, 5),     # 3: arrives 110 at 2 but departs before e[1] = 110
+             (0, 4, 100, 100),   # 4: e[4] = 200
+             (4, 5, 200, 0),     # 5: e[5] = 200
+             (5, 4, 200, 0)]     # 6: 5 -> 4 at the same instant (a cycle with 5)
+    a = np.array(conns, dtype=np.uint32)
+    u, v, dep, dur = a[:, 0], a[:, 1], a[:, 2], a[:, 3]
+    n, s, ts = 6, 0, 100
+    e_ok = [100, 110, 130, 150, 200, 200]
+    par_ok = [-1, 0, 1, 2, 4, 5]
+
+    def ok(e, par):
+        return oracle.witness_ok(n, u, v, dep, dur, s, ts, np.array(e, np.uint32), np.array(par, np.int64))
+
+    assert ok(e_ok, par_ok)
+    # the oracle's own parent output is this chain
+    e, par = oracle.csa(n, u, v, dep, dur, s, ts, with_parent=True)
+    assert e.tolist() == e_ok and ok(e, par)
+    bad = {
+        "parent into another vertex": (e_ok, [-1, 0, 2, 2, 4, 5]),
+        "departure before e[u] (1 -> 2 at 105 < e[1] = 110)": ([100, 110, 110, 150, 200, 200], [-1, 0, 3, 2, 4, 5]),
+        "arrival != dep + dur": ([100, 110, 130, 151, 200, 200], par_ok),
+        "cycle 4 <-> 5 never reaching s": (e_ok, [-1, 0, 1, 2, 6, 5]),
+        "finite e[x] without parent": (e_ok, [-1, 0, 1, -1, 4, 5]),
+        "INF vertex with a parent": ([100, 110, 130, INF, 200, 200], par_ok),
+        "e[s] != t_s": ([101, 110, 130, 150, 200, 200], par_ok),
+    }
+    for what, (e, par) in bad.items():
+        assert not ok(e, par), what
+
+
 def test_query_many_equals_single():
     rng = np.random.default_rng(9)
     n, m = 40, 2000
