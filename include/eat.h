@@ -46,7 +46,7 @@ extern "C" {
 #endif
 
 #define EAT_INF 0x7FFFFFFFu
-#define EAT_ABI_VERSION 2u
+#define EAT_ABI_VERSION 3u
 
 typedef enum eat_status {
     EAT_OK = 0,
@@ -163,6 +163,17 @@ typedef struct eat_build_opts {
                                      EAT_CONT_NONE = off (one hop per sweep, the paper's schedule),
                                      1..64 explicit; else EAT_EINVAL. */
     uint32_t exchange;            /* EDGE_PARTITIONED: EAT_EXCHANGE_ALLREDUCE (default) or EAT_EXCHANGE_PEER */
+    uint32_t local_sweeps;        /* EDGE_PARTITIONED + ALLREDUCE: at most this many local relaxation sweeps
+                                     per exchange round.  0 = sweep to local quiescence (default; fewest
+                                     rounds); 1 = the north star's literal schedule, one ncclAllReduce(min) of
+                                     e[] per sweep.  Results identical for every value. */
+    uint32_t num_devices;         /* REPLICATED: entries in `devices` (0 or 1: the single device `device`) */
+    const int32_t *devices;       /* REPLICATED with num_devices > 1: one index replica per listed CUDA device
+                                     (SURVEY 8(e) e1).  eat_query_many / eat_query_many_target shard the
+                                     queries in contiguous chunks, one host thread per device, each device
+                                     writing its own rows (no communication).  devices[0] is the primary:
+                                     every other call (single queries, *_device variants, stats) runs there.
+                                     Copied at build; caller may free it after eat_build returns. */
 } eat_build_opts;
 
 #define EAT_CONT_NONE 0xFFFFFFFFu
@@ -264,10 +275,24 @@ typedef struct eat_stats {
     uint64_t select_loop_cycles;  /*   ... slowest warp's own work inside the select phases (rest = barrier) */
     uint64_t pair_loop_cycles;    /*   ... slowest warp's own work inside the pair phases */
     uint32_t cta_grid;            /* resident CTAs (= queries in flight) of the batched CTA kernel; 0 if e[] does not fit */
-    uint32_t reserved0;
+    uint32_t num_devices;         /* devices holding a replica of this handle's index (1 unless eat_build_opts.devices) */
+    /* EAT_BUILD_COUNTERS only, for SURVEY 8(d)'s algorithmic bytes: */
+    uint64_t edge_evals;          /* (u,v) edges evaluated: first type of each distinct target in a vertex's type list */
+    uint64_t cluster_runs;        /* AP runs (count >= 2) held by the hour-cluster slots read */
+    uint64_t cluster_singles;     /* single departures (leftovers) held by the hour-cluster slots read */
+    uint64_t fallbacks;           /* lookups answered by the next non-empty cluster */
 } eat_stats;
 
 eat_status eat_get_stats(const eat_handle *h, eat_stats *out);
+
+/* Measurement utility (not a step of the EAT method): read d_buf (device
+ * memory, `bytes` a multiple of 16) `reps` times with 128-bit loads from a
+ * grid of (SM count x 8) CTAs of 256 threads, enqueued on cuda_stream.
+ * bench.py times it with CUDA events on a buffer that fits the L2 -- the
+ * measured L2-resident read bandwidth is the roofline peak of the batched
+ * kernel, whose index is L2-resident.  Errors: EAT_EINVAL
+ * (NULL / misaligned buffer), EAT_ECUDA. */
+eat_status eat_probe_read(const void *d_buf, uint64_t bytes, uint32_t reps, void *cuda_stream);
 
 /* Introspection of the packed index (host copy), for tests and tools.
  * Layout: vertices are internal ids; perm[c] is

@@ -33,7 +33,7 @@ EAT_PEER_HANDLE_BYTES = 64
 EXPORTED = ["eat_build", "eat_query", "eat_query_device", "eat_query_many", "eat_query_many_device",
             "eat_query_many_target", "eat_query_many_target_device",
             "eat_lookup_device", "eat_get_stats", "eat_index_export", "eat_index_sizes", "eat_partition_range", "eat_peer_export", "eat_peer_connect", "eat_free", "eat_last_error",
-            "eat_abi_version"]
+            "eat_abi_version", "eat_probe_read"]
 
 u32p = ctypes.POINTER(ctypes.c_uint32)
 
@@ -51,7 +51,9 @@ class eat_build_opts(ctypes.Structure):
                 ("nccl_unique_id", ctypes.c_void_p), ("window_seconds", ctypes.c_uint32),
                 ("cta_threads", ctypes.c_uint32), ("subtrips", ctypes.c_uint32),
                 ("arr_bits", ctypes.c_uint32), ("lookup", ctypes.c_uint32), ("cluster_dir", ctypes.c_uint32),
-                ("continuation", ctypes.c_uint32), ("exchange", ctypes.c_uint32)]
+                ("continuation", ctypes.c_uint32), ("exchange", ctypes.c_uint32),
+                ("local_sweeps", ctypes.c_uint32), ("num_devices", ctypes.c_uint32),
+                ("devices", ctypes.POINTER(ctypes.c_int32))]
 
 
 class eat_stats(ctypes.Structure):
@@ -68,7 +70,9 @@ class eat_stats(ctypes.Structure):
                 ("sweeps_total", ctypes.c_uint64), ("num_shortcuts", ctypes.c_uint64),
                 ("select_cycles", ctypes.c_uint64), ("pair_cycles", ctypes.c_uint64),
                 ("select_loop_cycles", ctypes.c_uint64), ("pair_loop_cycles", ctypes.c_uint64),
-                ("cta_grid", ctypes.c_uint32), ("reserved0", ctypes.c_uint32)]
+                ("cta_grid", ctypes.c_uint32), ("num_devices", ctypes.c_uint32),
+                ("edge_evals", ctypes.c_uint64), ("cluster_runs", ctypes.c_uint64),
+                ("cluster_singles", ctypes.c_uint64), ("fallbacks", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -128,6 +132,8 @@ def lib() -> ctypes.CDLL:
         L.eat_free.restype = None
         L.eat_last_error.argtypes = []
         L.eat_last_error.restype = ctypes.c_char_p
+        L.eat_probe_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p]
+        L.eat_probe_read.restype = S
         L.eat_abi_version.argtypes = []
         L.eat_abi_version.restype = ctypes.c_uint32
         _lib = L
@@ -216,6 +222,10 @@ def eat_free(h):
 
 def eat_last_error() -> str:
     return (lib().eat_last_error() or b"").decode(errors="replace")
+
+
+def eat_probe_read(d_buf: int, nbytes: int, reps: int, stream: int):
+    check(lib().eat_probe_read(d_buf, nbytes, reps, stream))
 
 
 def eat_abi_version() -> int:

@@ -61,7 +61,8 @@ cudaError_t dalloc_copy(T **dst, const T *src, size_t count, size_t &bytes) {
 // sources [lo, hi) (everything for a replicated handle).
 struct Slice {
     uint32_t lo = 0, hi = 0;
-    uint32_t *type_ptr = nullptr, *type_rec = nullptr, *crec = nullptr, *pool = nullptr, *type_src = nullptr;
+    uint32_t *type_ptr = nullptr, *type_hdr = nullptr, *type_cb = nullptr, *crec = nullptr, *pool = nullptr,
+             *type_src = nullptr;
     eat::DevIndex ix{};
     eat::PartWork pw{};
     uint64_t num_crec = 0, num_pool = 0;
@@ -136,6 +137,11 @@ struct eat_handle {
     eat::DevIndex *d_peer_ix = nullptr;
     eat::PeerLocal *d_peer_loc = nullptr;
     bool peer_ready = false;
+    // EDGE_PARTITIONED + ALLREDUCE: local sweeps per exchange round (0 = to quiescence)
+    uint32_t local_sweeps = 0;
+    // REPLICATED on several devices: replicas of this handle on devices[1..]
+    // (same index, own scratch); eat_query_many shards across {this} + replicas
+    std::vector<eat_handle *> replicas;
     // stats
     eat_stats st{};
 };
@@ -178,7 +184,7 @@ void release_device(eat_handle *h) {
         if (p) cudaFree(p);
     eat::async_free(h->aw);
     for (Slice &sl : h->slices) {
-        void *sp[] = {sl.type_ptr, sl.type_rec, sl.crec, sl.pool, sl.type_src};
+        void *sp[] = {sl.type_ptr, sl.type_hdr, sl.type_cb, sl.crec, sl.pool, sl.type_src};
         for (void *p : sp)
             if (p) cudaFree(p);
         eat::part_free(sl.pw);
@@ -231,19 +237,24 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
         uint32_t c = std::min(std::max(x.type_ptr[i], t_lo), t_hi);
         tptr[i] = c - t_lo;
     }
-    std::vector<uint32_t> trec(x.type_rec.begin() + uint64_t(t_lo) * eat::kTypeWords,
-                               x.type_rec.begin() + uint64_t(t_hi) * eat::kTypeWords);
-    std::vector<uint32_t> tsrc(T);
+    // device type records: 16-byte headers {v, lambda, first, last} (one
+    // 128-bit load), the cluster-record base crec_base - c_first in its own
+    // array (read only by lookups), the source in type_src (full sweep only);
+    // the host record's u and padding words never reach the device
+    std::vector<uint32_t> thdr(4 * T), tcb(T), tsrc(T);
     for (uint64_t t = 0; t < T; ++t) {
-        trec[t * eat::kTypeWords + 4] -= uint32_t(r_lo);
-        tsrc[t] = trec[t * eat::kTypeWords + 6];
+        const uint32_t *r = x.type_rec.data() + (uint64_t(t_lo) + t) * eat::kTypeWords;
+        for (int k = 0; k < 4; ++k) thdr[4 * t + k] = r[k];
+        tcb[t] = (r[4] - uint32_t(r_lo)) - r[5];  // mod 2^32: cb + k with k >= c_first stays in range
+        tsrc[t] = r[6];
     }
     std::vector<uint32_t> crec(x.crec.begin() + r_lo * eat::kCrecWords, x.crec.begin() + r_hi * eat::kCrecWords);
     for (uint64_t r = 0; r < r_hi - r_lo; ++r)
         if (crec[r * eat::kCrecWords + 1] == eat::kItemSpill) crec[r * eat::kCrecWords + 2] -= uint32_t(p_lo);
     size_t &b = h->index_bytes;
     CUDA_TRY(dalloc_copy(&sl.type_ptr, tptr.data(), tptr.size(), b));
-    CUDA_TRY(dalloc_copy(&sl.type_rec, trec.data(), trec.size(), b));
+    CUDA_TRY(dalloc_copy(&sl.type_hdr, thdr.data(), thdr.size(), b));
+    CUDA_TRY(dalloc_copy(&sl.type_cb, tcb.data(), tcb.size(), b));
     CUDA_TRY(dalloc_copy(&sl.crec, crec.data(), crec.size(), b));
     CUDA_TRY(dalloc_copy(&sl.pool, x.pool.data() + p_lo, p_hi - p_lo, b));
     CUDA_TRY(dalloc_copy(&sl.type_src, tsrc.data(), tsrc.size(), b));
@@ -262,7 +273,8 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     sl.ix.cta_threads = h->cta_threads;
     sl.ix.num_types = T;
     sl.ix.type_ptr = sl.type_ptr;
-    sl.ix.type_rec = reinterpret_cast<const uint4 *>(sl.type_rec);
+    sl.ix.type_hdr = reinterpret_cast<const uint4 *>(sl.type_hdr);
+    sl.ix.type_cb = sl.type_cb;
     sl.ix.crec = reinterpret_cast<const uint4 *>(sl.crec);
     sl.ix.pool = sl.pool;
     sl.ix.type_src = sl.type_src;
@@ -358,8 +370,10 @@ eat_status upload(eat_handle *h) {
     CUDA_TRY(cudaMalloc(&h->d_invalid, 8));
     CUDA_TRY(cudaMemset(h->d_invalid, 0, 8));
     if (h->mode == EAT_MODE_EDGE_PARTITIONED && h->exchange == EAT_EXCHANGE_ALLREDUCE)
-        for (Slice &sl : h->slices)
+        for (Slice &sl : h->slices) {
             if (eat::part_alloc(sl.pw, n) != cudaSuccess) return fail(EAT_ENOMEM, "cannot allocate partition scratch");
+            sl.pw.local_sweeps_per_round = h->local_sweeps;
+        }
     if (h->mode == EAT_MODE_EDGE_PARTITIONED && h->exchange == EAT_EXCHANGE_PEER) return peer_setup(h);
     return EAT_OK;
 }
@@ -400,8 +414,11 @@ eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_
         e = eat::part_query_loopback(ixs, ws, lo, hi, int(h->subwarp), s, t_s, d_out, st, &rounds, &sweeps, g_err);
     } else {
         Slice &sl = h->slices[0];
+        if (h->part_count > 1 && !h->comm)
+            return fail(EAT_ESTATE, "the NCCL communicator was aborted after an asynchronous error; rebuild the handle");
         e = eat::part_query(sl.ix, sl.pw, h->comm, sl.lo, sl.hi, int(h->subwarp), s, t_s, d_out, st, &rounds,
                             &sweeps, g_err);
+        if (sl.pw.comm_dead) h->comm = nullptr;  // ncclCommAbort freed it
     }
     if (e != EAT_OK) return e;
     h->st.last_rounds = rounds;
@@ -523,6 +540,81 @@ struct HandleOrder {
     ~HandleOrder() { cudaEventRecord(h->order_ev, st); }
 };
 
+
+// Option fields of a handle (validated); shared by the primary handle and
+// its replicas on other devices.
+eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
+    const uint32_t sw = o.subwarp == 0 ? 32u : (o.subwarp == 64 ? 0u : o.subwarp);  // 0 internally = flattened
+    if (sw != 0 && sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
+        return fail(EAT_EINVAL, "subwarp must be 0 (default 32), 1, 2, 4, 8, 16, 32 or 64 (flattened pairs)");
+    if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
+    if (o.kernel > EAT_KERNEL_BITMAP) return fail(EAT_EINVAL, "unknown kernel");
+    if (o.lookup > 2) return fail(EAT_EINVAL, "lookup must be 0 (Cluster-AP), 1 (Connection-type-AP) or 2 (linear)");
+    const uint32_t pc = o.part_count ? o.part_count : 1;
+    if (o.mode == EAT_MODE_EDGE_PARTITIONED && o.part_rank >= pc)
+        return fail(EAT_EINVAL, "edge partition needs part_rank < part_count");
+    h->subwarp = sw;
+    h->mode = o.mode;
+    h->window = o.window_seconds == 0 ? EAT_DEFAULT_WINDOW : o.window_seconds;
+    h->cta_threads = o.cta_threads == 0 ? 256u : o.cta_threads;
+    if (h->cta_threads != 512 && h->cta_threads != 384 && h->cta_threads != 256 && h->cta_threads != 192 &&
+        h->cta_threads != 128)
+        return fail(EAT_EINVAL, "cta_threads must be 128, 192, 256, 384 or 512");
+    if (o.arr_bits != 0 && o.arr_bits != 16 && o.arr_bits != 32) return fail(EAT_EINVAL, "arr_bits must be 0, 16 or 32");
+    h->arr16 = o.arr_bits == 16;
+    if (o.continuation != EAT_CONT_NONE && o.continuation > 64)
+        return fail(EAT_EINVAL, "continuation must be 0 (default 1), 1..64 or EAT_CONT_NONE");
+    h->cont_budget = o.continuation == 0 ? 1u : (o.continuation == EAT_CONT_NONE ? 0u : o.continuation);
+    if (const char *dv = getenv("EAT_E2E_DIRECT")) h->e2e_direct = atoi(dv) != 0;  // A/B (tools/e2e_ab.py)
+    h->part_rank = o.part_rank;
+    h->part_count = pc;
+    if (o.exchange > EAT_EXCHANGE_PEER) return fail(EAT_EINVAL, "exchange must be EAT_EXCHANGE_ALLREDUCE or EAT_EXCHANGE_PEER");
+    h->exchange = o.exchange;
+    if (o.local_sweeps && (o.mode != EAT_MODE_EDGE_PARTITIONED || o.exchange != EAT_EXCHANGE_ALLREDUCE))
+        return fail(EAT_EINVAL, "local_sweeps applies to EDGE_PARTITIONED handles with EAT_EXCHANGE_ALLREDUCE");
+    h->local_sweeps = o.local_sweeps;
+    // all partitions in this process (one device) unless this is one rank of
+    // several processes (NCCL id given, or EAT_BUILD_MULTIPROCESS for PEER)
+    h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 &&
+                  (o.exchange == EAT_EXCHANGE_PEER ? !(o.flags & EAT_BUILD_MULTIPROCESS) : !o.nccl_unique_id);
+    h->host_only = (o.flags & EAT_BUILD_HOST_ONLY) != 0;
+    h->lookup_mode = o.lookup;
+    return EAT_OK;
+}
+
+// Device part of eat_build on `device` (-1: current): stream, upload,
+// kernel choice, counters, NCCL communicator.  On error the caller releases.
+eat_status device_setup(eat_handle *h, const eat_build_opts &o, int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(EAT_ECUDA, "no CUDA device available (libeat has no CPU fallback)");
+    if (device >= 0) {
+        if (device >= ndev) return fail(EAT_EINVAL, "device ordinal out of range");
+        h->device = device;
+    } else {
+        cudaGetDevice(&h->device);
+    }
+    if (cudaSetDevice(h->device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(EAT_ECUDA, "cannot initialise CUDA device");
+    eat_status est = upload(h);
+    if (est != EAT_OK) return est;
+    if ((est = resolve_kernel(h, o.kernel)) != EAT_OK) return est;
+    if (o.flags & EAT_BUILD_COUNTERS) {
+        if (cudaMalloc(&h->d_work, eat::kWorkCounters * sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMemset(h->d_work, 0, eat::kWorkCounters * sizeof(unsigned long long)) != cudaSuccess)
+            return fail(EAT_ENOMEM, "cannot allocate work counters");
+    }
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED && !h->loopback && h->exchange == EAT_EXCHANGE_ALLREDUCE &&
+        h->part_count > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, o.nccl_unique_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&h->comm, int(h->part_count), id, int(o.part_rank));
+        if (r != ncclSuccess) return fail(EAT_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    return EAT_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -540,49 +632,27 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     p.renumber = o.renumber;
     if (o.cluster_dir > 2) return fail(EAT_EINVAL, "cluster_dir must be 0 (auto), 1 (dense) or 2 (compact)");
     p.dense = o.cluster_dir;
-    const uint32_t sw = o.subwarp == 0 ? 32u : (o.subwarp == 64 ? 0u : o.subwarp);  // 0 internally = flattened
-    if (sw != 0 && sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
-        return fail(EAT_EINVAL, "subwarp must be 0 (default 32), 1, 2, 4, 8, 16, 32 or 64 (flattened pairs)");
-    if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
-    if (o.kernel > EAT_KERNEL_BITMAP) return fail(EAT_EINVAL, "unknown kernel");
-    if (o.lookup > 2) return fail(EAT_EINVAL, "lookup must be 0 (Cluster-AP), 1 (Connection-type-AP) or 2 (linear)");
-    uint32_t pc = o.part_count ? o.part_count : 1;
-    if (o.mode == EAT_MODE_EDGE_PARTITIONED && o.part_rank >= pc)
-        return fail(EAT_EINVAL, "edge partition needs part_rank < part_count");
+    std::vector<int> devs;
+    if (o.num_devices > 1) {
+        if (!o.devices) return fail(EAT_EINVAL, "num_devices > 1 needs a devices array");
+        if (o.mode != EAT_MODE_REPLICATED)
+            return fail(EAT_EUNSUPPORTED, "several devices per handle: REPLICATED mode only (edge partitions are one rank per device)");
+        if (o.kernel == EAT_KERNEL_CONNECTION) return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CONNECTION is single-device");
+        for (uint32_t i = 0; i < o.num_devices; ++i) {
+            if (o.devices[i] < 0) return fail(EAT_EINVAL, "negative device ordinal");
+            for (int d : devs)
+                if (d == o.devices[i]) return fail(EAT_EINVAL, "device listed twice");
+            devs.push_back(o.devices[i]);
+        }
+        o.device = devs[0];
+    }
     eat_handle *h = new (std::nothrow) eat_handle();
     if (!h) return fail(EAT_ENOMEM, "out of host memory");
-    h->subwarp = sw;
-    h->mode = o.mode;
-    h->window = o.window_seconds == 0 ? EAT_DEFAULT_WINDOW : o.window_seconds;
-    h->cta_threads = o.cta_threads == 0 ? 256u : o.cta_threads;
-    if (h->cta_threads != 512 && h->cta_threads != 384 && h->cta_threads != 256 && h->cta_threads != 192 &&
-        h->cta_threads != 128) {
+    eat_status est = apply_opts(h, o);
+    if (est != EAT_OK) {
         delete h;
-        return fail(EAT_EINVAL, "cta_threads must be 128, 192, 256, 384 or 512");
+        return est;
     }
-    if (o.arr_bits != 0 && o.arr_bits != 16 && o.arr_bits != 32) {
-        delete h;
-        return fail(EAT_EINVAL, "arr_bits must be 0, 16 or 32");
-    }
-    h->arr16 = o.arr_bits == 16;
-    if (o.continuation != EAT_CONT_NONE && o.continuation > 64) {
-        delete h;
-        return fail(EAT_EINVAL, "continuation must be 0 (default 1), 1..64 or EAT_CONT_NONE");
-    }
-    h->cont_budget = o.continuation == 0 ? 1u : (o.continuation == EAT_CONT_NONE ? 0u : o.continuation);
-    if (const char *dv = getenv("EAT_E2E_DIRECT")) h->e2e_direct = atoi(dv) != 0;  // A/B (tools/e2e_ab.py)
-    h->part_rank = o.part_rank;
-    h->part_count = pc;
-    if (o.exchange > EAT_EXCHANGE_PEER) {
-        delete h;
-        return fail(EAT_EINVAL, "exchange must be EAT_EXCHANGE_ALLREDUCE or EAT_EXCHANGE_PEER");
-    }
-    h->exchange = o.exchange;
-    // all partitions in this process (one device) unless this is one rank of
-    // several processes (NCCL id given, or EAT_BUILD_MULTIPROCESS for PEER)
-    h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 &&
-                  (o.exchange == EAT_EXCHANGE_PEER ? !(o.flags & EAT_BUILD_MULTIPROCESS) : !o.nccl_unique_id);
-    h->host_only = (o.flags & EAT_BUILD_HOST_ONLY) != 0;
     std::string msg;
     int rc = EAT_OK;
     eat::SubtripStats sts;
@@ -613,7 +683,7 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
     s.num_clusters = h->hx.num_clusters;
     s.num_connections = tt->num_connections;
     s.num_shortcuts = sts.shortcuts;
-    h->lookup_mode = o.lookup;
+    s.num_devices = devs.empty() ? 1u : uint32_t(devs.size());
     if (o.kernel == EAT_KERNEL_CONNECTION && !h->host_only) {
         // Connection-version ablation (Alg. 4): keep the raw connections (internal ids)
         const uint64_t m = tt->num_connections;
@@ -631,51 +701,36 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
         *out = h;
         return EAT_OK;
     }
-    eat_status est = EAT_OK;
-    do {
-        int ndev = 0;
-        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-            est = fail(EAT_ECUDA, "no CUDA device available (libeat has no CPU fallback)");
+    est = device_setup(h, o, o.device);
+    // replicas on devices[1..] (REPLICATED, query sharding in eat_query_many):
+    // same options, a copy of the host index, their own device scratch
+    for (size_t i = 1; est == EAT_OK && i < devs.size(); ++i) {
+        eat_handle *r = new (std::nothrow) eat_handle();
+        if (!r) {
+            est = fail(EAT_ENOMEM, "out of host memory");
             break;
         }
-        if (o.device >= 0) {
-            if (o.device >= ndev) {
-                est = fail(EAT_EINVAL, "device ordinal out of range");
-                break;
-            }
-            h->device = o.device;
-        } else {
-            cudaGetDevice(&h->device);
-        }
-        if (cudaSetDevice(h->device) != cudaSuccess || cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
-            est = fail(EAT_ECUDA, "cannot initialise CUDA device");
+        h->replicas.push_back(r);
+        if ((est = apply_opts(r, o)) != EAT_OK) break;
+        try {
+            r->hx = h->hx;
+        } catch (const std::bad_alloc &) {
+            est = fail(EAT_ENOMEM, "out of host memory (replica index copy)");
             break;
         }
-        est = upload(h);
-        if (est != EAT_OK) break;
-        est = resolve_kernel(h, o.kernel);
-        if (est != EAT_OK) break;
-        if (o.flags & EAT_BUILD_COUNTERS) {
-            if (cudaMalloc(&h->d_work, 10 * sizeof(unsigned long long)) != cudaSuccess ||
-                cudaMemset(h->d_work, 0, 10 * sizeof(unsigned long long)) != cudaSuccess) {
-                est = fail(EAT_ENOMEM, "cannot allocate work counters");
-                break;
-            }
-        }
-        if (h->mode == EAT_MODE_EDGE_PARTITIONED && !h->loopback && h->exchange == EAT_EXCHANGE_ALLREDUCE) {
-            if (pc > 1) {
-                ncclUniqueId id;
-                std::memcpy(&id, o.nccl_unique_id, sizeof(id));
-                ncclResult_t r = ncclCommInitRank(&h->comm, int(pc), id, int(o.part_rank));
-                if (r != ncclSuccess) {
-                    est = fail(EAT_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
-                    break;
-                }
-            }
-        }
-    } while (0);
+        r->st = h->st;
+        est = device_setup(r, o, devs[i]);
+        // the replica serves device queries only: drop its host copy of the index
+        std::vector<uint32_t>().swap(r->hx.type_rec);
+        std::vector<uint32_t>().swap(r->hx.crec);
+        std::vector<uint32_t>().swap(r->hx.pool);
+    }
     if (est != EAT_OK) {
         std::string keep = g_err;
+        for (eat_handle *r : h->replicas) {
+            release_device(r);
+            delete r;
+        }
         release_device(h);
         delete h;
         g_err = keep;
@@ -687,6 +742,10 @@ eat_status eat_build(const eat_timetable *tt, const eat_build_opts *opts, eat_ha
 
 void eat_free(eat_handle *h) {
     if (!h) return;
+    for (eat_handle *r : h->replicas) {
+        release_device(r);
+        delete r;
+    }
     release_device(h);
     delete h;
 }
@@ -710,7 +769,7 @@ eat_status eat_get_stats(const eat_handle *hc, eat_stats *out) {
             h->st.last_rounds = rr;
         }
         if (h->d_work) {
-            unsigned long long w[10];
+            unsigned long long w[eat::kWorkCounters];
             CUDA_TRY(cudaMemcpy(w, h->d_work, sizeof(w), cudaMemcpyDeviceToHost));
             h->st.select_cycles = w[6];
             h->st.pair_cycles = w[7];
@@ -722,6 +781,10 @@ eat_status eat_get_stats(const eat_handle *hc, eat_stats *out) {
             h->st.spill_items_read = w[3];
             h->st.improvements = w[4];
             h->st.sweeps_total = w[5];
+            h->st.edge_evals = w[10];
+            h->st.cluster_runs = w[11];
+            h->st.cluster_singles = w[12];
+            h->st.fallbacks = w[13];
         }
     }
     *out = h->st;
@@ -768,6 +831,34 @@ eat_status eat_query(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *out_arr)
 }  // extern "C"
 
 namespace {
+
+eat_status query_targets_impl(eat_handle *h, const uint32_t *sources, const uint32_t *times, const uint32_t *dsts,
+                              uint64_t nq, uint32_t *out);
+
+// Run fn(handle, q0, count) for the query shards of a (possibly multi-device)
+// handle: contiguous chunks proportional to nothing but the device count
+// (replicas are identical), one host thread per device.  First error wins.
+template <class F>
+eat_status shard_queries(eat_handle *h, uint64_t nq, F fn) {
+    if (h->replicas.empty()) return fn(h, 0, nq);
+    std::vector<eat_handle *> hs{h};
+    hs.insert(hs.end(), h->replicas.begin(), h->replicas.end());
+    const uint64_t D = hs.size();
+    std::vector<eat_status> rc(D, EAT_OK);
+    std::vector<std::string> err(D);
+    std::vector<std::thread> th;
+    for (uint64_t d = 0; d < D; ++d) {
+        const uint64_t q0 = nq * d / D, q1 = nq * (d + 1) / D;
+        th.emplace_back([&, d, q0, q1] {
+            if (q1 > q0) rc[d] = fn(hs[d], q0, q1 - q0);
+            if (rc[d] != EAT_OK) err[d] = g_err;  // g_err is thread-local
+        });
+    }
+    for (auto &t : th) t.join();
+    for (uint64_t d = 0; d < D; ++d)
+        if (rc[d] != EAT_OK) return fail(rc[d], "device " + std::to_string(hs[d]->device) + ": " + err[d]);
+    return EAT_OK;
+}
 
 // Enqueue a batch of device-resident queries on st (CTA kernel), or, when e[]
 // does not fit shared memory, one single-query launch after another.
@@ -899,6 +990,17 @@ eat_status eat_query_many_target(eat_handle *h, const uint32_t *sources, const u
             return fail(EAT_EINVAL, "invalid source or destination vertex id at index " + std::to_string(q));
         if (times[q] >= EAT_INF) return fail(EAT_ERANGE, "t_s >= EAT_INF at index " + std::to_string(q));
     }
+    return shard_queries(h, nq, [&](eat_handle *hh, uint64_t q0, uint64_t c) {
+        return query_targets_impl(hh, sources + q0, times + q0, dsts + q0, c, out + q0);
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+eat_status query_targets_impl(eat_handle *h, const uint32_t *sources, const uint32_t *times, const uint32_t *dsts,
+                              uint64_t nq, uint32_t *out) {
     uint32_t *d = nullptr;
     {
         std::lock_guard<std::mutex> lk(h->mu);
@@ -919,18 +1021,8 @@ eat_status eat_query_many_target(eat_handle *h, const uint32_t *sources, const u
     return e;
 }
 
-eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t *times, uint64_t nq,
-                          uint32_t *out) {
-    if (!h) return fail(EAT_EINVAL, "NULL handle");
-    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
-    if (nq == 0) return EAT_OK;
-    if (!sources || !times || !out) return fail(EAT_EINVAL, "NULL argument");
-    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
-        return fail(EAT_ESTATE, "batched queries need a replicated handle (query-parallel sharding)");
-    for (uint64_t q = 0; q < nq; ++q) {
-        if (sources[q] >= h->hx.n) return fail(EAT_EINVAL, "invalid source vertex id at index " + std::to_string(q));
-        if (times[q] >= EAT_INF) return fail(EAT_ERANGE, "t_s >= EAT_INF at index " + std::to_string(q));
-    }
+eat_status query_many_impl(eat_handle *h, const uint32_t *sources, const uint32_t *times, uint64_t nq,
+                           uint32_t *out) {
     std::lock_guard<std::mutex> lk(h->mu);
     CUDA_TRY(cudaSetDevice(h->device));
     if (h->order_ev) CUDA_TRY(cudaEventSynchronize(h->order_ev));  // device calls still in flight
@@ -1030,6 +1122,28 @@ eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t
     return EAT_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+eat_status eat_query_many(eat_handle *h, const uint32_t *sources, const uint32_t *times, uint64_t nq,
+                          uint32_t *out) {
+    if (!h) return fail(EAT_EINVAL, "NULL handle");
+    if (h->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
+    if (nq == 0) return EAT_OK;
+    if (!sources || !times || !out) return fail(EAT_EINVAL, "NULL argument");
+    if (h->mode == EAT_MODE_EDGE_PARTITIONED)
+        return fail(EAT_ESTATE, "batched queries need a replicated handle (query-parallel sharding)");
+    for (uint64_t q = 0; q < nq; ++q) {
+        if (sources[q] >= h->hx.n) return fail(EAT_EINVAL, "invalid source vertex id at index " + std::to_string(q));
+        if (times[q] >= EAT_INF) return fail(EAT_ERANGE, "t_s >= EAT_INF at index " + std::to_string(q));
+    }
+    const uint64_t n = h->hx.n;
+    return shard_queries(h, nq, [&](eat_handle *hh, uint64_t q0, uint64_t c) {
+        return query_many_impl(hh, sources + q0, times + q0, c, out + q0 * n);
+    });
+}
+
 eat_status eat_lookup_device(eat_handle *h, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,
                              uint32_t *d_out, void *cuda_stream) {
     if (!h) return fail(EAT_EINVAL, "NULL handle");
@@ -1091,6 +1205,14 @@ eat_status eat_peer_connect(eat_handle *h, const void *handles, uint32_t count) 
     eat_status e = peer_publish(h);
     if (e != EAT_OK) return e;
     h->peer_ready = true;
+    return EAT_OK;
+}
+
+eat_status eat_probe_read(const void *d_buf, uint64_t bytes, uint32_t reps, void *cuda_stream) {
+    if (!d_buf || (reinterpret_cast<uintptr_t>(d_buf) & 15u) || (bytes & 15u))
+        return fail(EAT_EINVAL, "eat_probe_read: NULL or misaligned buffer");
+    CUDA_TRY(eat::launch_read_probe(static_cast<const uint4 *>(d_buf), bytes / 16, reps,
+                                    static_cast<cudaStream_t>(cuda_stream)));
     return EAT_OK;
 }
 

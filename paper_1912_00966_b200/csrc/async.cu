@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 1) k_query_async(DevIndex ix, A
                     const bool local = tr.v >= lo && tr.v < hi;
                     const uint32_t av = local ? vsarr[tr.v - lo] : ld_cg(w.garr + tr.v);
                     if (max(eu, tr.first) + tr.lam >= av) continue;
-                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, __ldg(ix.type_cb + t), eu);
                     const uint32_t cand = tc + tr.lam;
                     if (cand >= av) continue;
                     if (local) {

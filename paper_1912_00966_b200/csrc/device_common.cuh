@@ -68,10 +68,16 @@ __device__ __forceinline__ uint32_t cluster_scan(const DevIndex &ix, const uint4
     return best != kNone ? k * ix.cs + best : r0.x;
 }
 
-__device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t crec_base, uint32_t c_first,
-                                                   uint32_t eu) {
+// Record index base of type t: the record of its hour cluster k is cb + k
+// (compact directory: cb = crec_base - c_first from type_cb[]; dense
+// directory: cb = t * dense_nc, no load).
+__device__ __forceinline__ uint32_t type_cbase(const DevIndex &ix, uint64_t t) {
+    return ix.dense_nc ? uint32_t(t * ix.dense_nc) : __ldg(ix.type_cb + t);
+}
+
+__device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t cb, uint32_t eu) {
     const uint32_t k = cluster_of(ix, eu);
-    const uint64_t r = uint64_t(crec_base) + (k - c_first);
+    const uint64_t r = uint32_t(cb + k);
     const uint4 r0 = __ldg(ix.crec + 2 * r);
     const uint4 r1 = __ldg(ix.crec + 2 * r + 1);
     return cluster_scan(ix, r0, r1, k, eu);
@@ -95,21 +101,22 @@ __device__ __forceinline__ CrecPrefetch crec_prefetch(const DevIndex &ix, uint64
     return p;
 }
 
+// Connection-type header: one 16-byte load.
 struct TypeRec {
-    uint32_t v, lam, first, last, crec_base, c_first;
+    uint32_t v, lam, first, last;
 };
 
 __device__ __forceinline__ TypeRec load_type(const DevIndex &ix, uint64_t t) {
-    const uint4 a = __ldg(ix.type_rec + 2 * t);
-    const uint4 b = __ldg(ix.type_rec + 2 * t + 1);
-    return TypeRec{a.x, a.y, a.z, a.w, b.x, b.y};
+    const uint4 a = __ldg(ix.type_hdr + t);
+    return TypeRec{a.x, a.y, a.z, a.w};
 }
 
 // getConnection for one type (PAPER.md:226 semantics): first departure >= eu, or kInf.
-__device__ __forceinline__ uint32_t type_next_departure(const DevIndex &ix, const TypeRec &tr, uint32_t eu) {
+__device__ __forceinline__ uint32_t type_next_departure(const DevIndex &ix, uint64_t t, const TypeRec &tr,
+                                                        uint32_t eu) {
     if (eu > tr.last) return kInf;
     if (eu <= tr.first) return tr.first;
-    return cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+    return cluster_lookup(ix, type_cbase(ix, t), eu);
 }
 
 // Ablation lookups of the paper's incremental versions (NEXT-3), over the
@@ -120,13 +127,14 @@ __device__ __forceinline__ uint32_t type_next_departure(const DevIndex &ix, cons
 //     search over the departures in time order, stopping at the first >= e[u].
 enum { kLookupClusterAP = 0, kLookupAP = 1, kLookupLinear = 2 };
 
-__device__ __forceinline__ uint32_t type_lookup_ablation(const DevIndex &ix, const TypeRec &tr, uint32_t eu,
-                                                         uint32_t mode) {
+__device__ __forceinline__ uint32_t type_lookup_ablation(const DevIndex &ix, uint64_t t, const TypeRec &tr,
+                                                         uint32_t eu, uint32_t mode) {
     if (eu > tr.last) return kInf;  // early termination in every version
     uint32_t best = kInf;
     const uint32_t k0 = cluster_of(ix, tr.first), k1 = cluster_of(ix, tr.last);
+    const uint32_t cb = type_cbase(ix, t);
     for (uint32_t k = k0; k <= k1; ++k) {
-        const uint64_t r = uint64_t(tr.crec_base) + (k - tr.c_first);
+        const uint64_t r = uint32_t(cb + k);
         const uint4 r0 = __ldg(ix.crec + 2 * r), r1 = __ldg(ix.crec + 2 * r + 1);
         const bool spill = r0.y == kItemSpill;
         const uint32_t nitems = spill ? r0.w : uint32_t(kInlineItems);
@@ -232,10 +240,10 @@ __device__ __forceinline__ uint32_t relax_type_global(const DevIndex &ix, uint64
     if (eu > tr.last) return kNone;
     const uint32_t av = NO_AV ? kInf : __ldcg(arr + tr.v);
     if (max(eu, tr.first) + tr.lam >= av) return kNone;  // early termination
-    const uint32_t tc = ix.lookup_mode ? type_lookup_ablation(ix, tr, eu, ix.lookup_mode)
+    const uint32_t tc = ix.lookup_mode ? type_lookup_ablation(ix, t, tr, eu, ix.lookup_mode)
                         : eu <= tr.first ? tr.first
                                          : (ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
-                                                        : cluster_lookup(ix, tr.crec_base, tr.c_first, eu));
+                                                        : cluster_lookup(ix, __ldg(ix.type_cb + t), eu));
     if (tc == kInf) return kNone;
     const uint32_t cand = tc + tr.lam;
     if (cand >= av) return kNone;

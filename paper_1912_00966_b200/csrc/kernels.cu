@@ -69,8 +69,30 @@ namespace {
 __global__ void k_lookup(DevIndex ix, const uint32_t *type, const uint32_t *bound, uint64_t n, uint32_t *out) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         const TypeRec tr = load_type(ix, type[i]);
-        out[i] = type_next_departure(ix, tr, bound[i]);
+        out[i] = type_next_departure(ix, type[i], tr, bound[i]);
     }
+}
+
+// Instrumented variant only (SURVEY 8(d) algorithmic bytes): the contents of
+// the hour-cluster slot a lookup read -- AP runs (count >= 2) and single
+// departures -- and whether the answer came from the next non-empty cluster.
+__device__ __noinline__ void slot_census(const DevIndex &ix, uint32_t cb, uint32_t eu, uint32_t tc, uint32_t &runs,
+                                         uint32_t &singles, uint32_t &spill, uint32_t &fallback) {
+    const uint32_t k = cluster_of(ix, eu);
+    const uint64_t r = uint32_t(cb + k);
+    const uint4 r0 = __ldg(ix.crec + 2 * r), r1 = __ldg(ix.crec + 2 * r + 1);
+    auto one = [&](uint32_t it) {
+        if (it == kItemEmpty) return;
+        if ((it >> 24) > 0) ++runs;
+        else ++singles;
+    };
+    if (r0.y == kItemSpill) {
+        spill += r0.w;
+        for (uint32_t i = 0; i < r0.w; ++i) one(__ldg(ix.pool + r0.z + i));
+    } else {
+        one(r0.y), one(r0.z), one(r0.w), one(r1.x), one(r1.y), one(r1.z), one(r1.w);
+    }
+    if (tc != kInf && cluster_of(ix, tc) > k) ++fallback;
 }
 
 // ---------------------------------------------------------------- CTA kernel
@@ -239,6 +261,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
         const uint32_t di = TGT ? __ldg(ix.perm + dq) : 0u;
         uint32_t sweeps = 0;
         uint32_t c_vis = 0, c_type = 0, c_crec = 0, c_spill = 0, c_impr = 0;
+        uint32_t c_edge = 0, c_runs = 0, c_singles = 0, c_fb = 0;
         unsigned long long c_sel_cyc = 0, c_pair_cyc = 0, t_mark = COUNT ? clock64() : 0;
         unsigned long long c_sel_loop = 0, c_pair_loop = 0;  // slowest warp's own loop time
         if (COUNT && tid == 0) s_tw[0] = s_tw[1] = 0;
@@ -349,38 +372,72 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
                     const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
                     const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
+#ifndef EAT_SEGMIN
                     if (qp >= tot) continue;
+#endif
                     const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
-                    const uint32_t eu = ar.get(u);
-                    CrecPrefetch pf{};
-                    if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the type record
-                    const TypeRec tr = load_type(ix, t);
-                    if (COUNT) ++c_type;
-                    if (eu > tr.last) continue;
-                    const uint32_t av = ar.get(tr.v);
-                    const uint32_t lim = TGT ? min(av, ar.get(di)) : av;
-                    if (max(eu, tr.first) + tr.lam >= lim) continue;  // PAPER.md:411-416 (+ target bound)
-                    uint32_t tc;
-                    if (eu <= tr.first) {
-                        tc = tr.first;
-                    } else {
-                        tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu)
-                                         : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                    uint32_t cand = kInf, tv = 0;
+                    do {  // relax pair (u, t): leaves cand = kInf when it cannot improve e[v]
+                        if (qp >= tot) break;
+                        const uint32_t eu = ar.get(u);
+                        CrecPrefetch pf{};
+                        if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the header
+#ifndef EAT_CB_LAZY
+                        const uint32_t cb = ix.dense_nc ? 0u : __ldg(ix.type_cb + t);  // with the header
+#endif
+                        const TypeRec tr = load_type(ix, t);
                         if (COUNT) {
-                            ++c_crec;
-                            const uint4 rr = __ldg(ix.crec + 2ull * (tr.crec_base + cluster_of(ix, eu) - tr.c_first));
-                            if (rr.y == kItemSpill) c_spill += rr.w;
+                            ++c_type;
+                            if (t == o_p0 || __ldg(&ix.type_hdr[t - 1].x) != tr.v) ++c_edge;  // first type of (u,v)
                         }
+                        if (eu > tr.last) break;
+                        const uint32_t av = ar.get(tr.v);
+                        const uint32_t lim = TGT ? min(av, ar.get(di)) : av;
+                        if (max(eu, tr.first) + tr.lam >= lim) break;  // PAPER.md:411-416 (+ target bound)
+                        uint32_t tc;
+                        if (eu <= tr.first) {
+                            tc = tr.first;
+                        } else {
+#ifdef EAT_CB_LAZY
+                            const uint32_t cb = ix.dense_nc ? 0u : __ldg(ix.type_cb + t);
+#endif
+                            tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu) : cluster_lookup(ix, cb, eu);
+                            if (COUNT) {
+                                ++c_crec;
+                                slot_census(ix, ix.dense_nc ? uint32_t(t * ix.dense_nc) : cb, eu, tc, c_runs, c_singles,
+                                            c_spill, c_fb);
+                            }
+                        }
+                        if (tc + tr.lam < av) {
+                            cand = tc + tr.lam;
+                            tv = tr.v;
+                        }
+                    } while (false);
+#ifdef EAT_SEGMIN
+                    // segmented min over lanes with the same target (types of one
+                    // edge are adjacent lanes): the first lane of
+                    // each run of equal targets relaxes with the run's minimum
+                    {
+                        const uint32_t key = cand < kInf ? tv : (0x80000000u | lane);
+                        uint32_t m = cand;
+#pragma unroll
+                        for (uint32_t o = 1; o < 32; o <<= 1) {
+                            const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, m, o);
+                            const uint32_t ky = __shfl_down_sync(0xFFFFFFFFu, key, o);
+                            if (lane + o < 32u && ky == key) m = min(m, y);
+                        }
+                        const uint32_t kp = __shfl_up_sync(0xFFFFFFFFu, key, 1);
+                        if (lane > 0 && kp == key) continue;  // not the head of its run
+                        cand = m;
                     }
-                    const uint32_t cand = tc + tr.lam;
-                    if (cand < av) {
-                        const uint32_t old = ar.amin(tr.v, cand, &s_ovf);
-                        if (cand < old) {
-                            atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
-                            if (window < kInf) atomicMin(&s_tmin[t_nxt], cand);
-                            ++nimpr;
-                            if (COUNT) ++c_impr;
-                        }
+#endif
+                    if (cand >= kInf) continue;
+                    const uint32_t old = ar.amin(tv, cand, &s_ovf);
+                    if (cand < old) {
+                        atomicOr(bmN + (tv >> 5), 1u << (tv & 31u));
+                        if (window < kInf) atomicMin(&s_tmin[t_nxt], cand);
+                        ++nimpr;
+                        if (COUNT) ++c_impr;
                     }
                 }
             }
@@ -420,10 +477,11 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
         }
         if (tid == 0 && sweeps_out) sweeps_out[q] = sweeps;
         if (COUNT) {
-            unsigned long long v[5] = {c_vis, c_type, c_crec, c_spill, c_impr};
-            for (int k = 0; k < 5; ++k) {
+            unsigned long long v[9] = {c_vis, c_type, c_crec, c_spill, c_impr, c_edge, c_runs, c_singles, c_fb};
+            const int slot[9] = {0, 1, 2, 3, 4, 10, 11, 12, 13};
+            for (int k = 0; k < 9; ++k) {
                 for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o);
-                if (lane == 0 && v[k]) atomicAdd(counters + k, v[k]);
+                if (lane == 0 && v[k]) atomicAdd(counters + slot[k], v[k]);
             }
             if (tid == 0) {
                 atomicAdd(counters + 5, (unsigned long long)sweeps);
@@ -553,7 +611,7 @@ __device__ __forceinline__ void grid_solve(const DevIndex &ix, const GridWork &w
                     if (eu > tr.last) continue;
                     const uint32_t av = ld_cg(w.arr + tr.v);
                     if (max(eu, tr.first) + tr.lam >= av) continue;
-                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, tr.crec_base, tr.c_first, eu);
+                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, __ldg(ix.type_cb + t), eu);
                     const uint32_t cand = tc + tr.lam;
                     if (cand < av) {
                         const uint32_t old = atomicMin(w.arr + tr.v, cand);
@@ -917,6 +975,29 @@ size_t cta_static_smem() {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, k_query_cta<false, 1024, 2048, false, false>);
     return fa.sharedSizeBytes;
+}
+
+namespace {
+__device__ uint32_t g_probe_sink;
+
+// Streaming read of n 16-byte words, reps times (eat_probe_read).
+__global__ void __launch_bounds__(256) k_read_probe(const uint4 *__restrict__ p, uint64_t n, uint32_t reps) {
+    uint32_t acc = 0;
+    for (uint32_t r = 0; r < reps; ++r)
+        for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+            const uint4 v = __ldcg(p + i);
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    if (acc == 0x9E3779B9u) g_probe_sink = acc;  // keeps the loads alive
+}
+}  // namespace
+
+cudaError_t launch_read_probe(const uint4 *p, uint64_t n, uint32_t reps, cudaStream_t st) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    k_read_probe<<<unsigned(sms * 8), 256, 0, st>>>(p, n, reps);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,

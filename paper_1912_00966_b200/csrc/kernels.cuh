@@ -20,12 +20,20 @@ struct DevIndex {
     const uint4 *conns;         // [num_conns] {u, v, dep, arr} internal ids (EAT_KERNEL_CONNECTION only)
     uint64_t num_types;
     const uint32_t *type_ptr;   // [n+1]
-    const uint4 *type_rec;      // [2*T]  (32 B per type)
+    const uint4 *type_hdr;      // [T] 16-byte type headers {v, lambda, first_dep, last_dep}
+    const uint32_t *type_cb;    // [T] crec_base - c_first (mod 2^32): record of cluster k is type_cb[t] + k
     const uint4 *crec;          // [2*R]  (32 B per cluster record)
     const uint32_t *pool;       // spilled items
     const uint32_t *type_src;   // [T] internal source vertex per type (full-sweep schedule)
     const uint32_t *perm;       // [n] caller id -> internal id
 };
+
+// Work counters of the instrumented (EAT_BUILD_COUNTERS) batched kernel:
+// [0] vertex visits, [1] type headers read, [2] cluster slots read, [3]
+// spilled items read, [4] improvements, [5] sweeps, [6]-[9] select / pair
+// phase cycles (CTA kernel), [10] edge evaluations, [11] AP runs and [12]
+// single departures held by the slots read, [13] next-cluster fallbacks.
+constexpr int kWorkCounters = 14;
 
 // Control-word blocks (ctl) of the persistent kernels: kCtlWords words; the
 // grid-barrier counter sits alone on the second 128-byte line (kBarWord) so
@@ -47,6 +55,9 @@ enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2, kSchedConn = 3, kSche
 
 // Dynamic shared memory of the CTA kernel for n vertices (uint16 or uint32 e[]).
 size_t cta_smem_bytes(uint32_t n, bool a16);
+
+// Read-bandwidth probe (eat_probe_read): n 16-byte words, reps times.
+cudaError_t launch_read_probe(const uint4 *p, uint64_t n, uint32_t reps, cudaStream_t st);
 
 // Cluster-AP lookup for (type, bound) pairs (test entry point).
 cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,

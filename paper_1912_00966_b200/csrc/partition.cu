@@ -14,6 +14,7 @@
 // The fixpoint is the same as the single-GPU sweep's (relaxations commute
 // under min), so results are bit-identical.
 #include <algorithm>
+#include <thread>
 
 #include "device_common.cuh"
 #include "partition.cuh"
@@ -212,6 +213,30 @@ cudaError_t launch_gather(const DevIndex &ix, const uint32_t *arr, uint32_t *out
     return cudaGetLastError();
 }
 
+// Wait for stream st while polling the communicator for asynchronous
+// errors (a failed or aborted peer), so a rank never blocks forever in
+// cudaStreamSynchronize behind a collective that cannot complete.
+eat_status wait_polling(cudaStream_t st, ncclComm_t comm, std::string &err) {
+    for (uint64_t spin = 0;; ++spin) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e == cudaSuccess) return EAT_OK;
+        if (e != cudaErrorNotReady) {
+            err = std::string("round sync: ") + cudaGetErrorString(e);
+            return EAT_ECUDA;
+        }
+        if (comm && (spin & 63u) == 0) {
+            ncclResult_t ae = ncclSuccess;
+            const ncclResult_t r = ncclCommGetAsyncError(comm, &ae);
+            if (r != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress)) {
+                err = std::string("NCCL asynchronous error: ") + ncclGetErrorString(r != ncclSuccess ? r : ae);
+                ncclCommAbort(comm);  // unblocks the stream; the communicator is unusable afterwards
+                return EAT_ENCCL;
+            }
+        }
+        if (spin > 64) std::this_thread::yield();
+    }
+}
+
 eat_status part_query(const DevIndex &ix, PartWork &w, ncclComm_t comm, uint32_t lo, uint32_t hi, int subwarp,
                       uint32_t s, uint32_t t_s, uint32_t *d_out, cudaStream_t st, uint32_t *rounds, uint32_t *sweeps,
                       std::string &err) {
@@ -233,7 +258,11 @@ eat_status part_query(const DevIndex &ix, PartWork &w, ncclComm_t comm, uint32_t
         }
         if ((e = cudaMemcpyAsync(w.h_flag, w.arr + ix.n, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
             return cuda_fail(e, "flag copy");
-        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "round sync");
+        const eat_status ws = wait_polling(st, comm, err);
+        if (ws != EAT_OK) {
+            if (ws == EAT_ENCCL) w.comm_dead = true;
+            return ws;
+        }
         if (w.h_flag[0] == 1u) break;
         if (r > 4u * ix.n + 16u) {
             err = "edge-partitioned query did not converge";

@@ -24,6 +24,8 @@ struct PartWork {
     uint32_t n = 0;
     uint32_t h_sweeps = 0;       // sweeps of the last query (host copy)
     uint32_t local_sweeps_per_round = 0;  // 0 = to local quiescence; k = at most k sweeps per round
+                                          // (eat_build_opts.local_sweeps; 1 = one allreduce per sweep)
+    bool comm_dead = false;      // the communicator was aborted after an asynchronous NCCL error
 };
 
 cudaError_t part_alloc(PartWork &w, uint32_t n);

@@ -67,7 +67,8 @@ class Engine:
                  nccl_unique_id: Optional[bytes] = None, window: int = 0,
                  cta_threads: int = 0, subtrips: int = 0, trip=None, arr_bits: int = 0,
                  cluster_dir: str = "auto", lookup: str = "cluster_ap", continuation: Optional[int] = None,
-                 exchange: str = "allreduce", multiprocess: bool = False):
+                 exchange: str = "allreduce", multiprocess: bool = False, local_sweeps: int = 0,
+                 devices=None):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
@@ -83,6 +84,10 @@ class Engine:
         self._nccl_buf = None
         if nccl_unique_id is not None:
             self._nccl_buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+        self._devs = None
+        if devices is not None and len(devices) > 1:
+            self._devs = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
+            device = int(devices[0])
         opts = _lib.eat_build_opts(cluster_seconds=int(cluster_seconds), renumber=_lib.EAT_RENUMBER[renumber],
                                    device=int(device), kernel=_lib.EAT_KERNEL[kernel],
                                    flags=(_lib.EAT_BUILD_HOST_ONLY if host_only else 0)
@@ -95,7 +100,10 @@ class Engine:
                                    cluster_dir={"auto": 0, "dense": 1, "compact": 2}[cluster_dir],
                                    lookup={"cluster_ap": 0, "ap": 1, "linear": 2}[lookup],
                                    continuation=0 if continuation is None else (int(continuation) or _lib.EAT_CONT_NONE),
-                                   exchange=_lib.EAT_EXCHANGE[exchange])
+                                   exchange=_lib.EAT_EXCHANGE[exchange], local_sweeps=int(local_sweeps),
+                                   num_devices=len(self._devs) if self._devs is not None else 0,
+                                   devices=ctypes.cast(self._devs, ctypes.POINTER(ctypes.c_int32))
+                                   if self._devs is not None else None)
         self._h = _lib.eat_build(tt, opts)
         self.device = -1 if host_only else int(device)
         if self.device < 0 and not host_only:

@@ -30,5 +30,5 @@ def test_batch_workloads_table():
     import bench
 
     assert bench.BATCH_WORKLOADS["city_batch"][0] == "city"
-    assert bench.BATCH_WORKLOADS["city_batch"][1] == (1000, 10)  # 10k queries per GPU (BASELINE configs[2])
+    assert bench.BATCH_WORKLOADS["city_batch"][1] == (1000, 10)  # the one 10k batch of BASELINE configs[2]
     assert set(bench.SINGLE_WORKLOADS) == {"city_single", "metro_single", "country_part"}

@@ -354,6 +354,65 @@ def test_edge_partitioned_loopback(P):
         _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"loopback P={P} seed {seed}")
 
 
+@pytest.mark.parametrize("local_sweeps", [1, 2, 5])
+def test_edge_partitioned_bounded_rounds_loopback(local_sweeps):
+    """e2 with at most `local_sweeps` local sweeps per exchange round
+    (eat_build_opts.local_sweeps; 1 = the north star's one allreduce(min)
+    per sweep): vertices left on a bounded local frontier re-enter the next
+    round; e[] equals the oracle's and the round count grows as the bound
+    tightens."""
+    for name in ("tiny", "city"):
+        tt = synth.generate(name)
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        free = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=2)
+        eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=2, local_sweeps=local_sweeps)
+        rng = np.random.default_rng(local_sweeps)
+        qs = [synth.SINGLE_QUERY] + [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 86400))) for _ in range(3)]
+        for s, t_s in qs:
+            _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"bounded {local_sweeps} {name} ({s},{t_s})")
+        free.query(*synth.SINGLE_QUERY)
+        eng.query(*synth.SINGLE_QUERY)
+        assert eng.stats()["last_rounds"] >= free.stats()["last_rounds"]
+        if local_sweeps == 1:  # one exchange per sweep
+            assert eng.stats()["last_rounds"] >= eng.stats()["last_sweeps"] // 2
+    for seed in range(30):
+        tt = synth.random_small(3100 + seed)
+        eng = Engine.from_timetable(tt, mode="edge_partitioned", part_rank=0, part_count=[2, 3, 4][seed % 3],
+                                    local_sweeps=local_sweeps, subwarp=[32, 8, 1][seed % 3])
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        s, t_s = seed % tt.num_vertices, (seed * 7919) % (2 * 86400)
+        _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"bounded {local_sweeps} seed {seed}")
+    with pytest.raises(EatError) as e:  # replicated handles have no exchange rounds
+        Engine.from_timetable(synth.generate("tiny"), local_sweeps=1)
+    assert e.value.status == _lib.EAT_EINVAL
+
+
+def test_multi_device_handle():
+    """eat_build_opts.devices: one replica per listed
+    device, eat_query_many shards the batch over them in-library (one host
+    thread per device).  With one GPU the list is [0]; with two or more the
+    batch really spans devices.  Rows equal the oracle's."""
+    tt = synth.generate("tiny")
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    src, ts = synth.queries(tt, 50, 3)
+    want = csa.query_many(src, ts)
+    ndev = torch.cuda.device_count()
+    devs = list(range(min(ndev, 4)))
+    eng = Engine.from_timetable(tt, devices=devs)
+    assert eng.stats()["num_devices"] == len(devs)
+    _assert_rows(eng.query_many(src, ts), want, f"devices {devs}")
+    dst = (np.arange(src.size) * 13 % tt.num_vertices).astype(np.uint32)
+    assert np.array_equal(eng.query_targets(src, ts, dst), want[np.arange(src.size), dst])
+    _assert_rows(eng.query(*synth.SINGLE_QUERY), csa.query(*synth.SINGLE_QUERY), "multi-device handle single")
+    eng.close()
+    with pytest.raises(EatError) as e:
+        Engine.from_timetable(tt, devices=[0, 0])
+    assert e.value.status == _lib.EAT_EINVAL
+    with pytest.raises(EatError) as e:
+        Engine.from_timetable(tt, devices=[0, 1], mode="edge_partitioned", part_count=2)
+    assert e.value.status == _lib.EAT_EUNSUPPORTED
+
+
 @pytest.mark.parametrize("P", [1, 2, 3, 4, 8, 16])
 def test_edge_partitioned_peer_exchange_loopback(P):
     """NEXT-2 on one GPU: P edge partitions as P CTA groups of one launch, the

@@ -90,7 +90,10 @@ def _edge_protocol(rank, world):
     for i in np.nonzero(owned[tt.u])[0]:
         out_edges.setdefault(int(tt.u[i]), []).append((int(tt.v[i]), int(tt.dep[i]), int(tt.dur[i])))
     ok = True
-    for s, t_s in [(0, 21600), (57, 30000), (199, 80000)]:
+    # local_sweeps (eat_build_opts): 0 = local phase to quiescence; k = at
+    # most k sweeps per round, vertices left on the local frontier keep
+    # prev = INF (so they re-enter next round) and force another round
+    for local_sweeps, (s, t_s) in [(ls, q) for ls in (0, 1, 2) for q in [(0, 21600), (57, 30000), (199, 80000)]]:
         arr = np.full(n + 1, INF, dtype=np.int64)
         arr[s] = t_s
         prev = np.full(n, INF, dtype=np.int64)
@@ -99,7 +102,8 @@ def _edge_protocol(rank, world):
             rounds += 1
             work = [x for x in range(n) if owned[x] and arr[x] < prev[x]]
             remote = False
-            while work:
+            sweeps = 0
+            while work and not (local_sweeps and sweeps >= local_sweeps):
                 nxt = set()
                 for x in work:
                     for (v, d, lam) in out_edges.get(x, []):
@@ -110,8 +114,11 @@ def _edge_protocol(rank, world):
                             else:
                                 remote = True
                 work = sorted(nxt)
+                sweeps += 1
             prev[:] = arr[:n]
-            arr[n] = 0 if remote else 1
+            for x in work:  # left on a bounded local frontier
+                prev[x] = INF
+            arr[n] = 0 if (remote or work) else 1
             t = torch.from_numpy(arr.copy())
             dist.all_reduce(t, op=dist.ReduceOp.MIN)
             arr = t.numpy().astype(np.int64)
