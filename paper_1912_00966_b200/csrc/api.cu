@@ -123,6 +123,8 @@ struct eat_handle {
     int cta_grid = 0;
     uint32_t single_cta_threads = 1024;  // CTA variant of a lone query: 1024 when it fits, else cta_threads
     bool batch_groups = false;  // batches on k_query_groups even when e[] fits shared memory (kernel FRONTIER)
+    eat::SortScratch qsort[3];  // k_query_groups query order by source locality, per overflow/pipeline slot
+    bool sort_batches = true;   // EAT_SORT_BATCHES=0 disables (A/B)
     // edge partition
     uint32_t part_rank = 0, part_count = 1, part_lo = 0, part_hi = 0;
     ncclComm_t comm = nullptr;
@@ -183,6 +185,7 @@ void release_device(eat_handle *h) {
     for (void *p : ptrs)
         if (p) cudaFree(p);
     eat::async_free(h->aw);
+    for (eat::SortScratch &sc : h->qsort) eat::sort_scratch_free(sc);
     for (Slice &sl : h->slices) {
         void *sp[] = {sl.type_ptr, sl.type_hdr, sl.type_cb, sl.crec, sl.pool, sl.type_src};
         for (void *p : sp)
@@ -566,6 +569,7 @@ eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
         return fail(EAT_EINVAL, "continuation must be 0 (default 1), 1..64 or EAT_CONT_NONE");
     h->cont_budget = o.continuation == 0 ? 1u : (o.continuation == EAT_CONT_NONE ? 0u : o.continuation);
     if (const char *dv = getenv("EAT_E2E_DIRECT")) h->e2e_direct = atoi(dv) != 0;  // A/B (tools/e2e_ab.py)
+    if (const char *sv = getenv("EAT_SORT_BATCHES")) h->sort_batches = atoi(sv) != 0;  // A/B
     h->part_rank = o.part_rank;
     h->part_count = pc;
     if (o.exchange > EAT_EXCHANGE_PEER) return fail(EAT_EINVAL, "exchange must be EAT_EXCHANGE_ALLREDUCE or EAT_EXCHANGE_PEER");
@@ -900,7 +904,8 @@ eat_status launch_batch_cta(eat_handle *h, const uint32_t *d_sources, const uint
 // cooperative launch take queries in turn (k_query_groups); dst != NULL:
 // goal-directed, out[q] = e[dst[q]].
 eat_status launch_batch_groups(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
-                               uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, const uint32_t *d_dst) {
+                               uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, const uint32_t *d_dst,
+                               int slot) {
     uint32_t groups = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(kBatchGroupsMax, nq / 8)));
     // scratch is ~32 B per vertex per group: keep it under 4 GB
     groups = uint32_t(std::min<uint64_t>(groups, std::max<uint64_t>(1, (4ull << 30) / (32ull * h->hx.n + 1))));
@@ -917,15 +922,23 @@ eat_status launch_batch_groups(eat_handle *h, const uint32_t *d_sources, const u
         CUDA_TRY(cudaMalloc(&h->d_bgw, h->bgw.size() * sizeof(eat::GridWork)));
         CUDA_TRY(cudaMemcpy(h->d_bgw, h->bgw.data(), h->bgw.size() * sizeof(eat::GridWork), cudaMemcpyHostToDevice));
     }
+    // more queries than groups: hand them out in source-locality order
+    const uint32_t *qorder = nullptr;
+    if (h->sort_batches && nq > groups) {
+        eat::SortScratch &sc = h->qsort[slot];
+        if (sc.cap < nq) CUDA_TRY(cudaStreamSynchronize(st));
+        CUDA_TRY(eat::sort_queries_by_source(h->ix, d_sources, nq, sc, st));
+        qorder = sc.v1;
+    }
     CUDA_TRY(eat::launch_query_groups(h->ix, h->subwarp == 0 ? 32 : int(h->subwarp), h->bgw.data(), h->d_bgw, groups,
-                                      d_sources, d_times, nq, d_out, d_qcounter, h->d_invalid, d_dst, st));
+                                      d_sources, d_times, nq, d_out, d_qcounter, h->d_invalid, d_dst, qorder, st));
     return EAT_OK;
 }
 
 eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
                          uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, int slot = 0) {
     if (h->cta_grid > 0 && !h->batch_groups) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, d_qcounter, slot, nullptr);
-    return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, d_qcounter, nullptr);
+    return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, d_qcounter, nullptr, slot);
 }
 
 // Parallel host copy (staging -> caller memory).
@@ -976,7 +989,7 @@ eat_status eat_query_many_target_device(eat_handle *h, const uint32_t *d_sources
     HandleOrder order(h, st);
     if (h->cta_grid > 0 && !h->batch_groups) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, h->d_counter, 0, d_dsts);
     // e[] too large for shared memory: CTA groups, e[dst] of each query
-    return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, h->d_counter, d_dsts);
+    return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, h->d_counter, d_dsts, 0);
 }
 
 eat_status eat_query_many_target(eat_handle *h, const uint32_t *sources, const uint32_t *times, const uint32_t *dsts,

@@ -23,6 +23,8 @@
 #include <cuda/atomic>
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "device_common.cuh"
 #include "eat_internal.h"
 #include "kernels.cuh"
@@ -797,7 +799,8 @@ __global__ void __launch_bounds__(kGroupThreads, kGroupMinBlocks) k_query_groups
                                                                uint32_t *__restrict__ out,
                                                                unsigned long long *qcounter,
                                                                unsigned long long *invalid,
-                                                               const uint32_t *__restrict__ dstv) {
+                                                               const uint32_t *__restrict__ dstv,
+                                                               const uint32_t *__restrict__ qorder) {
     const uint32_t g = blockIdx.x / cpg, crank = blockIdx.x % cpg;
     const GridWork w = ws[g];
     const uint64_t gtid = crank * uint64_t(kGroupThreads) + threadIdx.x, gsz = uint64_t(cpg) * kGroupThreads;
@@ -811,7 +814,7 @@ __global__ void __launch_bounds__(kGroupThreads, kGroupMinBlocks) k_query_groups
         uint32_t *slot = w.ctl + 20 + (iter & 1u);
         if (gtid == 0) {
             const unsigned long long qi = atomicAdd(qcounter, 1ull);
-            *slot = qi < nq ? uint32_t(qi) : 0xFFFFFFFFu;
+            *slot = qi < nq ? (qorder ? qorder[qi] : uint32_t(qi)) : 0xFFFFFFFFu;
         }
         const uint32_t q = grid_sync(bar, epoch, cpg, slot);  // also: the previous row is written
         if (q == 0xFFFFFFFFu) break;
@@ -890,7 +893,7 @@ template <int SW>
 cudaError_t launch_groups_sw(const DevIndex &ix, const GridWork *h_ws, const GridWork *d_ws, uint32_t groups,
                              const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
                              unsigned long long *qcounter, unsigned long long *invalid, const uint32_t *dst,
-                             cudaStream_t st) {
+                             const uint32_t *qorder, cudaStream_t st) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -905,7 +908,7 @@ cudaError_t launch_groups_sw(const DevIndex &ix, const GridWork *h_ws, const Gri
     DevIndex ixc = ix;
     const GridWork *wp = d_ws;
     uint32_t c = cpg;
-    void *args[] = {&ixc, &wp, &c, &src, &ts, &nq, &out, &qcounter, &invalid, &dst};
+    void *args[] = {&ixc, &wp, &c, &src, &ts, &nq, &out, &qcounter, &invalid, &dst, &qorder};
     return cudaLaunchCooperativeKernel((const void *)k_query_groups<SW>, dim3(groups * cpg), dim3(kGroupThreads), args,
                                        0, st);
 }
@@ -1000,6 +1003,52 @@ cudaError_t launch_read_probe(const uint4 *p, uint64_t n, uint32_t reps, cudaStr
     return cudaGetLastError();
 }
 
+namespace {
+// Sort key of query q: its source's internal id (locality order), invalid
+// sources last.
+__global__ void k_query_keys(const uint32_t *__restrict__ perm, uint32_t n, const uint32_t *__restrict__ src,
+                             uint64_t nq, uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+    for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < nq; q += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t s = src[q];
+        keys[q] = s < n ? __ldg(perm + s) : n;
+        vals[q] = uint32_t(q);
+    }
+}
+}  // namespace
+
+cudaError_t sort_queries_by_source(const DevIndex &ix, const uint32_t *src, uint64_t nq, SortScratch &sc,
+                                   cudaStream_t st) {
+    if (nq > 0xFFFFFFFFull) return cudaErrorInvalidValue;
+    cudaError_t e;
+    if (sc.cap < nq) {
+        sort_scratch_free(sc);
+        size_t tmp = 0;
+        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                                 (uint32_t *)nullptr, (uint32_t *)nullptr, int(nq))) != cudaSuccess)
+            return e;
+        void **bufs[] = {(void **)&sc.k0, (void **)&sc.k1, (void **)&sc.v0, (void **)&sc.v1};
+        for (void **b : bufs)
+            if ((e = cudaMalloc(b, nq * 4)) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&sc.tmp, tmp)) != cudaSuccess) return e;
+        sc.tmp_bytes = tmp;
+        sc.cap = nq;
+    }
+    k_query_keys<<<unsigned(std::min<uint64_t>((nq + 255) / 256, 1184)), 256, 0, st>>>(ix.perm, ix.n, src, nq, sc.k0,
+                                                                                      sc.v0);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) <= ix.n) ++bits;
+    size_t tmp = sc.tmp_bytes;
+    return cub::DeviceRadixSort::SortPairs(sc.tmp, tmp, sc.k0, sc.k1, sc.v0, sc.v1, int(nq), 0, bits, st);
+}
+
+void sort_scratch_free(SortScratch &sc) {
+    void *p[] = {sc.k0, sc.k1, sc.v0, sc.v1, sc.tmp};
+    for (void *x : p)
+        if (x) cudaFree(x);
+    sc = SortScratch{};
+}
+
 cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,
                           uint32_t *d_out, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
@@ -1015,15 +1064,15 @@ cudaError_t launch_query_cta(const DevIndex &ix, const CtaArgs &a, cudaStream_t 
 cudaError_t launch_query_groups(const DevIndex &ix, int subwarp, const GridWork *h_ws, const GridWork *d_ws,
                                 uint32_t groups, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
                                 unsigned long long *qcounter, unsigned long long *invalid, const uint32_t *dst,
-                                cudaStream_t st) {
+                                const uint32_t *qorder, cudaStream_t st) {
     if (nq == 0) return cudaSuccess;
     switch (subwarp) {
-        case 1: return launch_groups_sw<1>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
-        case 2: return launch_groups_sw<2>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
-        case 4: return launch_groups_sw<4>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
-        case 8: return launch_groups_sw<8>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
-        case 16: return launch_groups_sw<16>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
-        default: return launch_groups_sw<32>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, st);
+        case 1: return launch_groups_sw<1>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, qorder, st);
+        case 2: return launch_groups_sw<2>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, qorder, st);
+        case 4: return launch_groups_sw<4>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, qorder, st);
+        case 8: return launch_groups_sw<8>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, qorder, st);
+        case 16: return launch_groups_sw<16>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, qorder, st);
+        default: return launch_groups_sw<32>(ix, h_ws, d_ws, groups, src, ts, nq, out, qcounter, invalid, dst, qorder, st);
     }
 }
 

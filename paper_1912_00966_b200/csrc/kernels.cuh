@@ -92,10 +92,25 @@ cudaError_t launch_query_grid(const DevIndex &ix, int subwarp, int sched, const 
 // cooperative launch, each with its own scratch (h_ws host copy / d_ws device
 // array of GridWork), solve the nq queries (frontier schedule); row q of out,
 // or out[q] = e[dst[q]] when dst != NULL (goal-directed).
+// qorder (optional, [nq]): the order in which groups take the queries.
 cudaError_t launch_query_groups(const DevIndex &ix, int subwarp, const GridWork *h_ws, const GridWork *d_ws,
                                 uint32_t groups, const uint32_t *src, const uint32_t *ts, uint64_t nq, uint32_t *out,
                                 unsigned long long *qcounter, unsigned long long *invalid, const uint32_t *dst,
-                                cudaStream_t st);
+                                const uint32_t *qorder, cudaStream_t st);
+
+// Query order by source locality (k_query_groups): v1[i] = the i-th query
+// when sorted by the internal id of its source (locality renumbering puts
+// nearby stops at nearby ids), so the CTA groups in flight at any time
+// explore overlapping parts of the index and share its L2 lines.
+struct SortScratch {
+    uint32_t *k0 = nullptr, *k1 = nullptr, *v0 = nullptr, *v1 = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    uint64_t cap = 0;
+};
+cudaError_t sort_queries_by_source(const DevIndex &ix, const uint32_t *src, uint64_t nq, SortScratch &sc,
+                                   cudaStream_t st);
+void sort_scratch_free(SortScratch &sc);
 
 // CTAs per SM of the persistent grid kernels (env EAT_GRID_CTAS_PER_SM, default 1).
 int grid_ctas_per_sm();
