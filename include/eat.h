@@ -285,6 +285,16 @@ typedef struct eat_stats {
 
 eat_status eat_get_stats(const eat_handle *h, eat_stats *out);
 
+/* Device self-test of the exactness assumptions behind two integer shortcuts
+ * of the kernels: (1) Algorithm 6's ceil-division ceil((e - start) / diff)
+ * computed in fp32 without integer fix-up, for every pair of
+ * 12-bit operands; (2) the hour cluster k = floor(e / cluster_seconds)
+ * computed by reciprocal multiplication with this handle's
+ * cluster width, for every e < 2^31.  failures[0], failures[1] receive the
+ * mismatch counts (0 on a correct device).  Errors: EAT_EINVAL (NULL),
+ * EAT_ESTATE (host-only handle), EAT_ECUDA. */
+eat_status eat_selftest(const eat_handle *h, uint64_t *failures);
+
 /* Measurement utility (not a step of the EAT method): read d_buf (device
  * memory, `bytes` a multiple of 16) `reps` times with 128-bit loads from a
  * grid of (SM count x 8) CTAs of 256 threads, enqueued on cuda_stream.

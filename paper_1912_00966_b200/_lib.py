@@ -33,7 +33,7 @@ EAT_PEER_HANDLE_BYTES = 64
 EXPORTED = ["eat_build", "eat_query", "eat_query_device", "eat_query_many", "eat_query_many_device",
             "eat_query_many_target", "eat_query_many_target_device",
             "eat_lookup_device", "eat_get_stats", "eat_index_export", "eat_index_sizes", "eat_partition_range", "eat_peer_export", "eat_peer_connect", "eat_free", "eat_last_error",
-            "eat_abi_version", "eat_probe_read"]
+            "eat_abi_version", "eat_probe_read", "eat_selftest"]
 
 u32p = ctypes.POINTER(ctypes.c_uint32)
 
@@ -132,8 +132,12 @@ def lib() -> ctypes.CDLL:
         L.eat_free.restype = None
         L.eat_last_error.argtypes = []
         L.eat_last_error.restype = ctypes.c_char_p
-        L.eat_probe_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p]
-        L.eat_probe_read.restype = S
+        if hasattr(L, "eat_probe_read"):  # (older builds under A/B lack the ABI-3 utilities)
+            L.eat_probe_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p]
+            L.eat_probe_read.restype = S
+        if hasattr(L, "eat_selftest"):
+            L.eat_selftest.argtypes = [H, ctypes.POINTER(ctypes.c_uint64)]
+            L.eat_selftest.restype = S
         L.eat_abi_version.argtypes = []
         L.eat_abi_version.restype = ctypes.c_uint32
         _lib = L
@@ -226,6 +230,12 @@ def eat_last_error() -> str:
 
 def eat_probe_read(d_buf: int, nbytes: int, reps: int, stream: int):
     check(lib().eat_probe_read(d_buf, nbytes, reps, stream))
+
+
+def eat_selftest(h):
+    f = (ctypes.c_uint64 * 2)()
+    check(lib().eat_selftest(h, f))
+    return int(f[0]), int(f[1])
 
 
 def eat_abi_version() -> int:

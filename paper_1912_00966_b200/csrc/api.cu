@@ -1221,6 +1221,25 @@ eat_status eat_peer_connect(eat_handle *h, const void *handles, uint32_t count) 
     return EAT_OK;
 }
 
+eat_status eat_selftest(const eat_handle *hc, uint64_t *failures) {
+    if (!hc || !failures) return fail(EAT_EINVAL, "NULL argument");
+    if (hc->host_only) return fail(EAT_ESTATE, "handle was built with EAT_BUILD_HOST_ONLY");
+    eat_handle *h = const_cast<eat_handle *>(hc);
+    std::lock_guard<std::mutex> lk(h->mu);
+    CUDA_TRY(cudaSetDevice(h->device));
+    unsigned long long *d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+    cudaError_t e = eat::launch_selftest(h->ix, d, h->stream);
+    unsigned long long f[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(f, d, sizeof(f), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFree(d);
+    CUDA_TRY(e);
+    failures[0] = f[0];
+    failures[1] = f[1];
+    return EAT_OK;
+}
+
 eat_status eat_probe_read(const void *d_buf, uint64_t bytes, uint32_t reps, void *cuda_stream) {
     if (!d_buf || (reinterpret_cast<uintptr_t>(d_buf) & 15u) || (bytes & 15u))
         return fail(EAT_EINVAL, "eat_probe_read: NULL or misaligned buffer");

@@ -15,6 +15,16 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
 
+// ceil(a / s) for 1 <= a, s < 2^12 (Algorithm 6's ceil-div):
+// floor((a + s - 0.5) / s) in fp32 with the approximate reciprocal (MUFU.RCP,
+// relative error < 2^-21).  The exact quotient (a + s - 0.5)/s lies at least
+// 0.5/s from every integer while the rounding error is below 8191 * 2^-21 / s,
+// so the floor is exact -- no integer fix-up (checked exhaustively on the
+// device by eat_selftest).
+__device__ __forceinline__ uint32_t ceil_div12(uint32_t a, uint32_t s) {
+    return __float2uint_rd(__fdividef(__uint2float_rn(a + s) - 0.5f, __uint2float_rn(s)));
+}
+
 // First term >= x of one packed AP item, as an offset inside the cluster;
 // kNone if the item is empty or all its terms are < x.  Algorithm 6 lines 3-8
 // (PAPER.md:288-294): x <= start -> start; start < x <= end ->
@@ -25,14 +35,7 @@ __device__ __forceinline__ uint32_t item_next(uint32_t it, uint32_t x) {
     if (x <= off) return off;
     const uint32_t last = off + cm1 * stride;
     if (x > last) return kNone;  // also covers singletons (cm1 == 0): stride unused
-    // ceil((x - off) / stride) for 12-bit operands: float estimate of the
-    // floor (error < 1), then an exact integer fix-up
-    const uint32_t a = x - off;
-    uint32_t q = __float2uint_rz(__fdividef(__uint2float_rz(a), __uint2float_rz(stride)));  // MUFU.RCP-based
-    int32_t r = int32_t(a) - int32_t(q * stride);
-    if (r < 0) { --q; r += int32_t(stride); }
-    if (r >= int32_t(stride)) { ++q; r -= int32_t(stride); }
-    return off + (q + (r != 0 ? 1u : 0u)) * stride;
+    return off + ceil_div12(x - off, stride) * stride;
 }
 
 // Hour cluster of time e (k = e[u]/3600): exact reciprocal
@@ -75,12 +78,41 @@ __device__ __forceinline__ uint32_t type_cbase(const DevIndex &ix, uint64_t t) {
     return ix.dense_nc ? uint32_t(t * ix.dense_nc) : __ldg(ix.type_cb + t);
 }
 
+// Same lookup from the record's address: the second half of the record
+// (items 3-6) is loaded only when the first three items do not decide --
+// most hour clusters hold one or two APs.
 __device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t cb, uint32_t eu) {
     const uint32_t k = cluster_of(ix, eu);
     const uint64_t r = uint32_t(cb + k);
     const uint4 r0 = __ldg(ix.crec + 2 * r);
-    const uint4 r1 = __ldg(ix.crec + 2 * r + 1);
-    return cluster_scan(ix, r0, r1, k, eu);
+    if (r0.y == kItemSpill) return cluster_scan(ix, r0, r0, k, eu);
+    const uint32_t x = eu - k * ix.cs;
+    uint32_t best = kNone;
+    bool more = true;
+    const uint32_t a[3] = {r0.y, r0.z, r0.w};
+#pragma unroll
+    for (int i = 0; i < 3 && more; ++i) {
+        if (a[i] == kItemEmpty) {
+            more = false;
+        } else {
+            best = min(best, item_next(a[i], x));
+            more = (a[i] & 0xFFFu) < x;  // items sorted by first term
+        }
+    }
+    if (more) {
+        const uint4 r1 = __ldg(ix.crec + 2 * r + 1);
+        const uint32_t b[4] = {r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+        for (int i = 0; i < 4 && more; ++i) {
+            if (b[i] == kItemEmpty) {
+                more = false;
+            } else {
+                best = min(best, item_next(b[i], x));
+                more = (b[i] & 0xFFFu) < x;
+            }
+        }
+    }
+    return best != kNone ? k * ix.cs + best : r0.x;
 }
 
 // Dense cluster directory (ix.dense_nc > 0): the record of (type t, cluster

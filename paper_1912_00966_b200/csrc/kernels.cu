@@ -267,12 +267,14 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
         unsigned long long c_sel_cyc = 0, c_pair_cyc = 0, t_mark = COUNT ? clock64() : 0;
         unsigned long long c_sel_loop = 0, c_pair_loop = 0;  // slowest warp's own loop time
         if (COUNT && tid == 0) s_tw[0] = s_tw[1] = 0;
+        // rotating s_tmin slots: t_cur = sweep % 3 (this sweep's window base),
+        // t_nxt = (sweep + 1) % 3 (written by this sweep), t_old = (sweep + 2) % 3
+        uint32_t t_cur = 0, t_nxt = 1, t_old = 2;
         for (;;) {
             const uint32_t p = sweeps & 1u;
-            const uint32_t t_nxt = (sweeps + 1u) % 3u;  // s_tmin slot written by this sweep
             uint32_t thr = kInf;
             if (window < kInf) {
-                const uint32_t base = s_tmin[sweeps % 3u];
+                const uint32_t base = s_tmin[t_cur];
                 thr = base + min(window, kInf - base);  // saturating
             }
             // goal-directed: a vertex with e[u] >= e[dst] cannot lower e[dst]
@@ -337,14 +339,14 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             if (tid == 0) {  // slots of the next sweep: everyone is past their last read
                 s_cnt[p ^ 1u] = 0;
                 s_more[p ^ 1u] = 0;
-                s_tmin[(sweeps + 2u) % 3u] = kInf;
+                s_tmin[t_old] = kInf;
             }
             const uint32_t F = min(s_cnt[p], uint32_t(kListCap));
             // ---- 2. warp-level flattened (vertex, type) pairs; a warp takes g
             // consecutive list entries so that small frontiers still spread
             // over all warps
             const uint32_t g = min(32u, max(1u, (F + kCtaWarps - 1u) / kCtaWarps));
-            uint32_t nimpr = 0;
+            uint32_t nimpr = 0, imin = kInf;  // improvements; their minimum feeds the next window base
             for (uint32_t k0 = wid * g; k0 < F; k0 += kCtaWarps * g) {
                 const uint32_t j = k0 + lane;
                 uint32_t x = 0, p0 = 0, nt = 0;
@@ -374,78 +376,56 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
                     const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
                     const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
-#ifndef EAT_SEGMIN
                     if (qp >= tot) continue;
-#endif
                     const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
-                    uint32_t cand = kInf, tv = 0;
-                    do {  // relax pair (u, t): leaves cand = kInf when it cannot improve e[v]
-                        if (qp >= tot) break;
-                        const uint32_t eu = ar.get(u);
-                        CrecPrefetch pf{};
-                        if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the header
-#ifndef EAT_CB_LAZY
-                        const uint32_t cb = ix.dense_nc ? 0u : __ldg(ix.type_cb + t);  // with the header
-#endif
-                        const TypeRec tr = load_type(ix, t);
-                        if (COUNT) {
-                            ++c_type;
-                            if (t == o_p0 || __ldg(&ix.type_hdr[t - 1].x) != tr.v) ++c_edge;  // first type of (u,v)
-                        }
-                        if (eu > tr.last) break;
-                        const uint32_t av = ar.get(tr.v);
-                        const uint32_t lim = TGT ? min(av, ar.get(di)) : av;
-                        if (max(eu, tr.first) + tr.lam >= lim) break;  // PAPER.md:411-416 (+ target bound)
-                        uint32_t tc;
-                        if (eu <= tr.first) {
-                            tc = tr.first;
-                        } else {
-#ifdef EAT_CB_LAZY
-                            const uint32_t cb = ix.dense_nc ? 0u : __ldg(ix.type_cb + t);
-#endif
-                            tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu) : cluster_lookup(ix, cb, eu);
-                            if (COUNT) {
-                                ++c_crec;
-                                slot_census(ix, ix.dense_nc ? uint32_t(t * ix.dense_nc) : cb, eu, tc, c_runs, c_singles,
-                                            c_spill, c_fb);
-                            }
-                        }
-                        if (tc + tr.lam < av) {
-                            cand = tc + tr.lam;
-                            tv = tr.v;
-                        }
-                    } while (false);
-#ifdef EAT_SEGMIN
-                    // segmented min over lanes with the same target (types of one
-                    // edge are adjacent lanes): the first lane of
-                    // each run of equal targets relaxes with the run's minimum
-                    {
-                        const uint32_t key = cand < kInf ? tv : (0x80000000u | lane);
-                        uint32_t m = cand;
-#pragma unroll
-                        for (uint32_t o = 1; o < 32; o <<= 1) {
-                            const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, m, o);
-                            const uint32_t ky = __shfl_down_sync(0xFFFFFFFFu, key, o);
-                            if (lane + o < 32u && ky == key) m = min(m, y);
-                        }
-                        const uint32_t kp = __shfl_up_sync(0xFFFFFFFFu, key, 1);
-                        if (lane > 0 && kp == key) continue;  // not the head of its run
-                        cand = m;
+                    const uint32_t eu = ar.get(u);
+                    CrecPrefetch pf{};
+                    if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the header
+                    // the cluster base goes out with the header (a lazy load after
+                    // the early-termination tests costs -5 %: one more dependent hop,
+                    // profiles/r02_ab_type_hdr16_segmin.jsonl)
+                    const uint32_t cb = ix.dense_nc ? 0u : __ldg(ix.type_cb + t);
+                    const TypeRec tr = load_type(ix, t);
+                    if (COUNT) {
+                        ++c_type;
+                        if (t == o_p0 || __ldg(&ix.type_hdr[t - 1].x) != tr.v) ++c_edge;  // first type of (u,v)
                     }
-#endif
-                    if (cand >= kInf) continue;
-                    const uint32_t old = ar.amin(tv, cand, &s_ovf);
-                    if (cand < old) {
-                        atomicOr(bmN + (tv >> 5), 1u << (tv & 31u));
-                        if (window < kInf) atomicMin(&s_tmin[t_nxt], cand);
-                        ++nimpr;
-                        if (COUNT) ++c_impr;
+                    if (eu > tr.last) continue;
+                    const uint32_t av = ar.get(tr.v);
+                    const uint32_t lim = TGT ? min(av, ar.get(di)) : av;
+                    if (max(eu, tr.first) + tr.lam >= lim) continue;  // PAPER.md:411-416 (+ target bound)
+                    uint32_t tc;
+                    if (eu <= tr.first) {
+                        tc = tr.first;
+                    } else {
+                        tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu) : cluster_lookup(ix, cb, eu);
+                        if (COUNT) {
+                            ++c_crec;
+                            slot_census(ix, ix.dense_nc ? uint32_t(t * ix.dense_nc) : cb, eu, tc, c_runs, c_singles,
+                                        c_spill, c_fb);
+                        }
+                    }
+                    // (a segmented min over lanes sharing the target before the
+                    // shared atomicMin costs 10 %: r02_ab_type_hdr16_segmin.jsonl)
+                    const uint32_t cand = tc + tr.lam;
+                    if (cand < av) {
+                        const uint32_t old = ar.amin(tr.v, cand, &s_ovf);
+                        if (cand < old) {
+                            atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
+                            imin = min(imin, cand);
+                            ++nimpr;
+                            if (COUNT) ++c_impr;
+                        }
                     }
                 }
             }
             if (COUNT && lane == 0) atomicMax(&s_tw[1], clock64() - t_pr0);
             nimpr = __reduce_add_sync(0xFFFFFFFFu, nimpr);
             if (lane == 0 && nimpr) atomicAdd(&s_more[p], nimpr);
+            if (window < kInf) {
+                imin = __reduce_min_sync(0xFFFFFFFFu, imin);
+                if (lane == 0 && imin < kInf) atomicMin(&s_tmin[t_nxt], imin);
+            }
             __syncthreads();
             if (COUNT && tid == 0) {
                 const unsigned long long now = clock64();
@@ -455,6 +435,12 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                 s_tw[1] = 0;
             }
             ++sweeps;
+            {
+                const uint32_t tmp = t_cur;
+                t_cur = t_nxt;
+                t_nxt = t_old;
+                t_old = tmp;
+            }
             if (s_more[p] == 0u) break;  // nothing deferred, nothing lowered: fixpoint
             if (A16 && s_ovf) break;      // recomputed by the uint32 variant
         }
@@ -1047,6 +1033,34 @@ void sort_scratch_free(SortScratch &sc) {
     for (void *x : p)
         if (x) cudaFree(x);
     sc = SortScratch{};
+}
+
+namespace {
+// eat_selftest: (1) ceil_div12 == integer ceil for every 1 <= a, s < 2^12;
+// (2) cluster_of(e) == e / cs for every e < 2^31 (this index's cs).
+__global__ void k_selftest(DevIndex ix, unsigned long long *fail) {
+    const uint64_t gtid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x, gsz = uint64_t(gridDim.x) * blockDim.x;
+    unsigned long long f0 = 0, f1 = 0;
+    for (uint64_t i = gtid; i < (1ull << 24); i += gsz) {
+        const uint32_t a = uint32_t(i >> 12), st = uint32_t(i & 0xFFFu);
+        if (a == 0 || st == 0) continue;
+        if (ceil_div12(a, st) != (a + st - 1u) / st) ++f0;
+    }
+    for (uint64_t e = gtid; e < (1ull << 31); e += gsz)
+        if (cluster_of(ix, uint32_t(e)) != uint32_t(e) / ix.cs) ++f1;
+    if (f0) atomicAdd(fail, f0);
+    if (f1) atomicAdd(fail + 1, f1);
+}
+}  // namespace
+
+cudaError_t launch_selftest(const DevIndex &ix, unsigned long long *d_fail, cudaStream_t st) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaMemsetAsync(d_fail, 0, 2 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    k_selftest<<<unsigned(sms * 8), 256, 0, st>>>(ix, d_fail);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_lookup(const DevIndex &ix, const uint32_t *d_type, const uint32_t *d_bound, uint64_t n,

@@ -56,6 +56,9 @@ enum { kSchedFrontier = 0, kSchedFull = 1, kSchedFlat = 2, kSchedConn = 3, kSche
 // Dynamic shared memory of the CTA kernel for n vertices (uint16 or uint32 e[]).
 size_t cta_smem_bytes(uint32_t n, bool a16);
 
+// Exactness self-test of ceil_div12 and cluster_of (eat_selftest): d_fail[0..1] mismatch counts.
+cudaError_t launch_selftest(const DevIndex &ix, unsigned long long *d_fail, cudaStream_t st);
+
 // Read-bandwidth probe (eat_probe_read): n 16-byte words, reps times.
 cudaError_t launch_read_probe(const uint4 *p, uint64_t n, uint32_t reps, cudaStream_t st);
 

@@ -206,6 +206,10 @@ class Engine:
                                _stream_ptr(stream))
         return out
 
+    def selftest(self):
+        """(ceil-div mismatches, cluster-index mismatches) on this device (eat_selftest; 0, 0 expected)."""
+        return _lib.eat_selftest(self._h)
+
     def peer_export(self) -> bytes:
         """This rank's exchange-block handle (EAT_EXCHANGE_PEER, multiprocess)."""
         return _lib.eat_peer_export(self._h)

@@ -73,6 +73,17 @@ def test_lookup_kernel_vs_get_connection(name, cs):
     _assert_rows(out.cpu().numpy().astype(np.uint32), np.array(want, np.uint32), f"lookup {name} cs={cs}")
 
 
+def test_device_selftest():
+    """eat_selftest: the fp32 ceil-division of Algorithm 6 (every 12-bit
+    operand pair) and the reciprocal-multiply hour cluster (every e < 2^31,
+    for several cluster widths) are exact on this device."""
+    tt = synth.generate("tiny")
+    for cs in (3600, 1, 7, 60, 900, 4095, 4096):
+        eng = Engine.from_timetable(tt, cluster_seconds=cs)
+        assert eng.selftest() == (0, 0), cs
+        eng.close()
+
+
 # ----------------------------------------------------------------------------- single queries
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("subwarp", [0, 1, 8, 64])
