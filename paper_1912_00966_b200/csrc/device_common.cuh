@@ -78,41 +78,15 @@ __device__ __forceinline__ uint32_t type_cbase(const DevIndex &ix, uint64_t t) {
     return ix.dense_nc ? uint32_t(t * ix.dense_nc) : __ldg(ix.type_cb + t);
 }
 
-// Same lookup from the record's address: the second half of the record
-// (items 3-6) is loaded only when the first three items do not decide --
-// most hour clusters hold one or two APs.
+// Lookup from the record index: both halves of the 32-byte record are
+// requested at once (loading items 3-6 only when items 0-2 do not decide
+// costs 4 % on the city batch: profiles/r02_ab_lazy_crec_half.jsonl).
 __device__ __forceinline__ uint32_t cluster_lookup(const DevIndex &ix, uint32_t cb, uint32_t eu) {
     const uint32_t k = cluster_of(ix, eu);
     const uint64_t r = uint32_t(cb + k);
     const uint4 r0 = __ldg(ix.crec + 2 * r);
-    if (r0.y == kItemSpill) return cluster_scan(ix, r0, r0, k, eu);
-    const uint32_t x = eu - k * ix.cs;
-    uint32_t best = kNone;
-    bool more = true;
-    const uint32_t a[3] = {r0.y, r0.z, r0.w};
-#pragma unroll
-    for (int i = 0; i < 3 && more; ++i) {
-        if (a[i] == kItemEmpty) {
-            more = false;
-        } else {
-            best = min(best, item_next(a[i], x));
-            more = (a[i] & 0xFFFu) < x;  // items sorted by first term
-        }
-    }
-    if (more) {
-        const uint4 r1 = __ldg(ix.crec + 2 * r + 1);
-        const uint32_t b[4] = {r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-        for (int i = 0; i < 4 && more; ++i) {
-            if (b[i] == kItemEmpty) {
-                more = false;
-            } else {
-                best = min(best, item_next(b[i], x));
-                more = (b[i] & 0xFFFu) < x;
-            }
-        }
-    }
-    return best != kNone ? k * ix.cs + best : r0.x;
+    const uint4 r1 = __ldg(ix.crec + 2 * r + 1);
+    return cluster_scan(ix, r0, r1, k, eu);
 }
 
 // Dense cluster directory (ix.dense_nc > 0): the record of (type t, cluster
