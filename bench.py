@@ -78,7 +78,8 @@ def _init_dist():
 
         backend = os.environ.get("EAT_BENCH_BACKEND", "nccl")
         if backend == "nccl":
-            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines show the N ranks
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines show the N ranks ...
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # ... on stderr: stdout is the JSON line
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)

@@ -281,6 +281,7 @@ typedef struct eat_stats {
     uint64_t cluster_runs;        /* AP runs (count >= 2) held by the hour-cluster slots read */
     uint64_t cluster_singles;     /* single departures (leftovers) held by the hour-cluster slots read */
     uint64_t fallbacks;           /* lookups answered by the next non-empty cluster */
+    uint64_t select_bits;         /* active (deferred or new) vertices examined by the CTA kernel's select phases */
 } eat_stats;
 
 eat_status eat_get_stats(const eat_handle *h, eat_stats *out);

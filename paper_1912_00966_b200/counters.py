@@ -23,7 +23,7 @@ from __future__ import annotations
 import numpy as np
 
 KEYS = ("vertex_visits", "type_evals", "cluster_reads", "spill_items_read", "improvements", "sweeps_total",
-        "edge_evals", "cluster_runs", "cluster_singles", "fallbacks")
+        "edge_evals", "cluster_runs", "cluster_singles", "fallbacks", "select_bits")
 
 
 def algorithmic_bytes(c: dict, nq: int, n: int) -> int:

@@ -266,6 +266,7 @@ eat_status upload_slice(eat_handle *h, uint32_t lo, uint32_t hi, Slice &sl) {
     sl.ix.dense_nc = x.dense_nc;
     sl.ix.lookup_mode = h->lookup_mode;
     sl.ix.cont_budget = h->cont_budget;
+    sl.ix.zero = 0;
     {
         uint32_t l = 0;
         while ((1u << l) < x.cs) ++l;  // ceil(log2 cs)
@@ -789,6 +790,7 @@ eat_status eat_get_stats(const eat_handle *hc, eat_stats *out) {
             h->st.cluster_runs = w[11];
             h->st.cluster_singles = w[12];
             h->st.fallbacks = w[13];
+            h->st.select_bits = w[14];
         }
     }
     *out = h->st;

@@ -22,8 +22,11 @@ __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p);
 // so the floor is exact -- no integer fix-up (checked exhaustively on the
 // device by eat_selftest).
 __device__ __forceinline__ uint32_t ceil_div12(uint32_t a, uint32_t s) {
-    return __float2uint_rd(__fdividef(__uint2float_rn(a + s) - 0.5f, __uint2float_rn(s)));
+    float r;  // approximate reciprocal (MUFU.RCP), no range fix-up: s is a small integer
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__uint2float_rn(s)));
+    return __float2uint_rd((__uint2float_rn(a + s) - 0.5f) * r);
 }
+
 
 // First term >= x of one packed AP item, as an offset inside the cluster;
 // kNone if the item is empty or all its terms are < x.  Algorithm 6 lines 3-8

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
         const uint32_t di = TGT ? __ldg(ix.perm + dq) : 0u;
         uint32_t sweeps = 0;
         uint32_t c_vis = 0, c_type = 0, c_crec = 0, c_spill = 0, c_impr = 0;
-        uint32_t c_edge = 0, c_runs = 0, c_singles = 0, c_fb = 0;
+        uint32_t c_edge = 0, c_runs = 0, c_singles = 0, c_fb = 0, c_selbits = 0;
         unsigned long long c_sel_cyc = 0, c_pair_cyc = 0, t_mark = COUNT ? clock64() : 0;
         unsigned long long c_sel_loop = 0, c_pair_loop = 0;  // slowest warp's own loop time
         if (COUNT && tid == 0) s_tw[0] = s_tw[1] = 0;
@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             for (uint32_t w = tid; w < W; w += kCtaThreads) {
                 uint32_t word = bmD[w] | bmN[w];
                 if (!word) continue;
+                if (COUNT) c_selbits += __popc(word);
                 bmN[w] = 0;
                 uint32_t sel = word;
                 if (thr < kInf || (TGT && best < kInf)) {
@@ -363,6 +364,9 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     if (lane >= uint32_t(o)) incl += y;
                 }
                 const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                // (measured alternatives, profiles/r02_ab_owner_search_variants.jsonl:
+                // a start-bitmask + shared-memory owner map -1 %, e[u] read once per
+                // chunk and shuffled -2 %: the per-pair read sees fresher arrivals)
                 for (uint32_t base = 0; base < tot; base += 32u) {
                     const uint32_t qp = base + lane;
                     // owner lane: smallest L with incl[L] > qp
@@ -379,13 +383,17 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     if (qp >= tot) continue;
                     const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
                     const uint32_t eu = ar.get(u);
-                    CrecPrefetch pf{};
-                    if (ix.dense_nc) pf = crec_prefetch(ix, t, eu);  // in parallel with the header
                     // the cluster base goes out with the header (a lazy load after
                     // the early-termination tests costs -5 %: one more dependent hop,
-                    // profiles/r02_ab_type_hdr16_segmin.jsonl)
-                    const uint32_t cb = ix.dense_nc ? 0u : __ldg(ix.type_cb + t);
-                    const TypeRec tr = load_type(ix, t);
+                    // profiles/r02_ab_type_hdr16_segmin.jsonl).  type_cb also holds
+                    // t * dense_nc for a dense directory, so this kernel has no
+                    // per-pair directory branch (the speculative record prefetch of
+                    // the grid kernels, relax_type_global, is latency-bound work)
+                    const uint32_t cb = __ldg(ix.type_cb + t);
+                    TypeRec tr = load_type(ix, t);
+                    // the first test consumes cb (& 0, a runtime zero): the compiler
+                    // would otherwise sink its load into the lookup branch
+                    tr.last |= cb & ix.zero;
                     if (COUNT) {
                         ++c_type;
                         if (t == o_p0 || __ldg(&ix.type_hdr[t - 1].x) != tr.v) ++c_edge;  // first type of (u,v)
@@ -398,11 +406,10 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     if (eu <= tr.first) {
                         tc = tr.first;
                     } else {
-                        tc = ix.dense_nc ? cluster_scan(ix, pf.r0, pf.r1, pf.k, eu) : cluster_lookup(ix, cb, eu);
+                        tc = cluster_lookup(ix, cb, eu);
                         if (COUNT) {
                             ++c_crec;
-                            slot_census(ix, ix.dense_nc ? uint32_t(t * ix.dense_nc) : cb, eu, tc, c_runs, c_singles,
-                                        c_spill, c_fb);
+                            slot_census(ix, cb, eu, tc, c_runs, c_singles, c_spill, c_fb);
                         }
                     }
                     // (a segmented min over lanes sharing the target before the
@@ -465,9 +472,10 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
         }
         if (tid == 0 && sweeps_out) sweeps_out[q] = sweeps;
         if (COUNT) {
-            unsigned long long v[9] = {c_vis, c_type, c_crec, c_spill, c_impr, c_edge, c_runs, c_singles, c_fb};
-            const int slot[9] = {0, 1, 2, 3, 4, 10, 11, 12, 13};
-            for (int k = 0; k < 9; ++k) {
+            unsigned long long v[10] = {c_vis, c_type, c_crec, c_spill, c_impr, c_edge, c_runs, c_singles, c_fb,
+                                        c_selbits};
+            const int slot[10] = {0, 1, 2, 3, 4, 10, 11, 12, 13, 14};
+            for (int k = 0; k < 10; ++k) {
                 for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o);
                 if (lane == 0 && v[k]) atomicAdd(counters + slot[k], v[k]);
             }

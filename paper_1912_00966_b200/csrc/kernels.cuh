@@ -16,6 +16,7 @@ struct DevIndex {
     uint32_t dense_nc;          // > 0: dense cluster directory, record (t, k) at t*dense_nc + k
     uint32_t lookup_mode;       // 0 Cluster-AP; ablations (grid kernels): 1 Connection-type-AP, 2 Connection-type linear
     uint32_t cont_budget;       // grid frontier kernel: extra vertices a sub-warp relaxes in the same sweep (continuation)
+    uint32_t zero;              // always 0 (a value the compiler cannot fold: pins a load's issue point)
     uint64_t num_conns;         // connection-version schedule: raw connections on the device
     const uint4 *conns;         // [num_conns] {u, v, dep, arr} internal ids (EAT_KERNEL_CONNECTION only)
     uint64_t num_types;
@@ -32,8 +33,9 @@ struct DevIndex {
 // [0] vertex visits, [1] type headers read, [2] cluster slots read, [3]
 // spilled items read, [4] improvements, [5] sweeps, [6]-[9] select / pair
 // phase cycles (CTA kernel), [10] edge evaluations, [11] AP runs and [12]
-// single departures held by the slots read, [13] next-cluster fallbacks.
-constexpr int kWorkCounters = 14;
+// single departures held by the slots read, [13] next-cluster fallbacks,
+// [14] active vertices examined by the select phases.
+constexpr int kWorkCounters = 15;
 
 // Control-word blocks (ctl) of the persistent kernels: kCtlWords words; the
 // grid-barrier counter sits alone on the second 128-byte line (kBarWord) so

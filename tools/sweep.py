@@ -76,7 +76,8 @@ def main():
                 torch.cuda.synchronize()
                 st = e2.stats()
                 rec["per_query"] = {k: st[k] / src.size for k in (
-                    "vertex_visits", "type_evals", "edge_evals", "cluster_reads", "improvements", "sweeps_total")}
+                    "vertex_visits", "type_evals", "edge_evals", "cluster_reads", "improvements", "sweeps_total",
+                    "select_bits")}
                 sw = max(1, st["sweeps_total"])
                 rec["cycles_per_sweep"] = {"phase": st["select_cycles"] / sw, "select_loop": st["select_loop_cycles"] / sw,
                                            "pair_loop": st["pair_loop_cycles"] / sw}
