@@ -120,6 +120,14 @@ struct eat_handle {
     uint32_t *d_dsrc = nullptr, *d_dts = nullptr;
     uint64_t dcap = 0;
     bool e2e_direct = true;
+    // streamed mode (pinned output, batched CTA kernel): rows go to device
+    // memory; per-chunk completion flags in mapped host memory let the host
+    // copy finished chunks with the copy engine while the kernel still runs
+    int e2e_mode = 1;                 // 0 chunk pipeline, 1 direct (kernel stores into mapped host rows), 2 streamed (-1.5 %: profiles/r02_e2e_modes.jsonl)
+    uint32_t *d_srows = nullptr;      // [scap][n] device rows
+    uint64_t scap = 0;
+    unsigned int *h_done = nullptr, *d_done = nullptr;  // mapped per-query finished flags
+    uint64_t done_cap = 0;
     int cta_grid = 0;
     uint32_t single_cta_threads = 1024;  // CTA variant of a lone query: 1024 when it fits, else cta_threads
     bool batch_groups = false;  // batches on k_query_groups even when e[] fits shared memory (kernel FRONTIER)
@@ -178,6 +186,8 @@ void release_device(eat_handle *h) {
     gridwork_free(h->gw);
     for (eat::GridWork &w : h->bgw) gridwork_free(w);
     if (h->d_bgw) cudaFree(h->d_bgw);
+    if (h->d_srows) cudaFree(h->d_srows);
+    if (h->h_done) cudaFreeHost(h->h_done);
     void *ptrs[] = {h->d_perm,  h->d_out1, h->d_q1,      h->d_sweeps1,  h->d_counter,  h->d_invalid,
                     h->d_bsrc[0], h->d_bts[0], h->d_bout[0], h->d_bsrc[1], h->d_bts[1], h->d_bout[1],
                     h->d_bcounter, h->d_work, h->d_rounds1, h->d_ovf[0], h->d_ovf[1], h->d_ovf[2],
@@ -569,7 +579,8 @@ eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
     if (o.continuation != EAT_CONT_NONE && o.continuation > 64)
         return fail(EAT_EINVAL, "continuation must be 0 (default 1), 1..64 or EAT_CONT_NONE");
     h->cont_budget = o.continuation == 0 ? 1u : (o.continuation == EAT_CONT_NONE ? 0u : o.continuation);
-    if (const char *dv = getenv("EAT_E2E_DIRECT")) h->e2e_direct = atoi(dv) != 0;  // A/B (tools/e2e_ab.py)
+    if (const char *dv = getenv("EAT_E2E_DIRECT")) h->e2e_direct = atoi(dv) != 0;  // A/B
+    if (const char *mv = getenv("EAT_E2E_MODE")) h->e2e_mode = atoi(mv);            // A/B: 0 pipeline, 1 direct, 2 streamed
     if (const char *sv = getenv("EAT_SORT_BATCHES")) h->sort_batches = atoi(sv) != 0;  // A/B
     h->part_rank = o.part_rank;
     h->part_count = pc;
@@ -1036,6 +1047,81 @@ eat_status query_targets_impl(eat_handle *h, const uint32_t *sources, const uint
     return e;
 }
 
+// Streamed batch into page-locked host rows (caller holds h->mu): one
+// persistent CTA-kernel launch writes rows to device memory and counts each
+// finished row in its chunk's flag (mapped host memory); this thread copies
+// every completed chunk with the copy engine (cudaMemcpyAsync on a second
+// stream) while the kernel keeps relaxing later queries.  Queries are taken
+// in order, so chunks complete roughly in order; the tail is one chunk.
+eat_status query_many_streamed(eat_handle *h, const uint32_t *sources, const uint32_t *times, uint64_t nq,
+                               uint32_t *out) {
+    const uint64_t n = h->hx.n;
+    constexpr uint32_t kShift = 8;  // 256 queries (10 MB of city rows) per chunk
+    const uint64_t nch = (nq + (1u << kShift) - 1) >> kShift;
+    if (!h->bstream[0])
+        for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&h->bstream[i], cudaStreamNonBlocking));
+    if (!h->d_bcounter) CUDA_TRY(cudaMalloc(&h->d_bcounter, 2 * sizeof(unsigned long long)));
+    if (h->dcap < nq) {
+        if (h->d_dsrc) cudaFree(h->d_dsrc);
+        if (h->d_dts) cudaFree(h->d_dts);
+        h->d_dsrc = h->d_dts = nullptr;
+        h->dcap = 0;
+        CUDA_TRY(cudaMalloc(&h->d_dsrc, nq * 4));
+        CUDA_TRY(cudaMalloc(&h->d_dts, nq * 4));
+        h->dcap = nq;
+    }
+    if (h->scap < nq) {
+        if (h->d_srows) cudaFree(h->d_srows);
+        h->d_srows = nullptr;
+        h->scap = 0;
+        CUDA_TRY(cudaMalloc(&h->d_srows, nq * n * 4));
+        h->scap = nq;
+    }
+    if (h->done_cap < nq) {
+        if (h->h_done) cudaFreeHost(h->h_done);
+        h->h_done = nullptr;
+        h->done_cap = 0;
+        CUDA_TRY(cudaHostAlloc(&h->h_done, nq * sizeof(unsigned int), cudaHostAllocMapped));
+        CUDA_TRY(cudaHostGetDevicePointer(&h->d_done, h->h_done, 0));
+        h->done_cap = nq;
+    }
+    std::memset(h->h_done, 0, nq * sizeof(unsigned int));
+    cudaStream_t ks = h->bstream[0], cs = h->bstream[1];
+    CUDA_TRY(cudaMemcpyAsync(h->d_dsrc, sources, nq * 4, cudaMemcpyHostToDevice, ks));
+    CUDA_TRY(cudaMemcpyAsync(h->d_dts, times, nq * 4, cudaMemcpyHostToDevice, ks));
+    eat::CtaArgs a;
+    a.src = h->d_dsrc;
+    a.ts = h->d_dts;
+    a.nq = nq;
+    a.out = h->d_srows;
+    a.qcounter = h->d_bcounter;
+    a.invalid = h->d_invalid;
+    a.threads = int(h->cta_threads);
+    a.done = h->d_done;
+    CUDA_TRY(eat::launch_query_cta(h->ix, a, ks));
+    const volatile unsigned int *flags = h->h_done;
+    uint64_t seen = 0;  // rows [0, seen) are known finished
+    for (uint64_t c = 0; c < nch; ++c) {
+        const uint64_t q0 = c << kShift, q1 = std::min<uint64_t>(q0 + (uint64_t(1) << kShift), nq);
+        for (uint64_t spin = 0; seen < q1; ++spin) {
+            if (flags[seen]) {
+                ++seen;
+                continue;
+            }
+            if ((spin & 1023u) == 1023u) {  // a failed kernel never finishes the chunk
+                const cudaError_t ke = cudaStreamQuery(ks);
+                if (ke != cudaSuccess && ke != cudaErrorNotReady) return fail(EAT_ECUDA, cudaGetErrorString(ke));
+                if (ke == cudaSuccess && !flags[seen]) return fail(EAT_ECUDA, "streamed batch: row not flagged");
+                std::this_thread::yield();
+            }
+        }
+        CUDA_TRY(cudaMemcpyAsync(out + q0 * n, h->d_srows + q0 * n, (q1 - q0) * n * 4, cudaMemcpyDeviceToHost, cs));
+    }
+    CUDA_TRY(cudaStreamSynchronize(ks));
+    CUDA_TRY(cudaStreamSynchronize(cs));
+    return EAT_OK;
+}
+
 eat_status query_many_impl(eat_handle *h, const uint32_t *sources, const uint32_t *times, uint64_t nq,
                            uint32_t *out) {
     std::lock_guard<std::mutex> lk(h->mu);
@@ -1049,7 +1135,9 @@ eat_status query_many_impl(eat_handle *h, const uint32_t *sources, const uint32_
     cudaPointerAttributes pa{};
     const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    if (pinned && pa.devicePointer && h->e2e_direct) {
+    if (pinned && h->e2e_mode == 2 && h->cta_grid > 0 && !h->batch_groups && !h->arr16 && !h->d_work)
+        return query_many_streamed(h, sources, times, nq, out);
+    if (pinned && pa.devicePointer && h->e2e_direct && h->e2e_mode != 0) {
         // Direct: one persistent launch over all queries; each CTA (or CTA
         // group) stores its finished rows into the page-locked host buffer
         // over PCIe (mapped pointer), so the D2H traffic overlaps the

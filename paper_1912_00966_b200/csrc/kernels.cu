@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                                                                const uint32_t *__restrict__ qlist,
                                                                const uint32_t *__restrict__ qcount,
                                                                uint32_t *__restrict__ ovf_list,
-                                                               uint32_t *__restrict__ ovf_cnt) {
+                                                               uint32_t *__restrict__ ovf_cnt,
+                                                               unsigned int *done) {
     constexpr uint32_t kCtaWarps = kCtaThreads / 32;
     extern __shared__ uint32_t sm[];
     const uint32_t n = ix.n;
@@ -235,6 +236,11 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             if (tid == 0) {
                 atomicAdd(invalid, 1ull);
                 if (sweeps_out) sweeps_out[q] = 0;
+            }
+            if (done) {
+                __threadfence_system();
+                __syncthreads();
+                if (tid == 0) *reinterpret_cast<volatile unsigned int *>(done + q) = 1u;
             }
             __syncthreads();
             continue;
@@ -486,6 +492,16 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                 atomicAdd(counters + 8, c_sel_loop);
                 atomicAdd(counters + 9, c_pair_loop);
             }
+        }
+        if (done) {
+            // streamed e2e (eat_query_many, page-locked output): flag the
+            // finished row in mapped host memory once every thread's row
+            // stores are visible system-wide (one plain store per query: no
+            // atomics on host memory, which PCIe hosts need not support); the
+            // host copies a chunk as soon as all its rows are flagged
+            __threadfence_system();
+            __syncthreads();
+            if (tid == 0) *reinterpret_cast<volatile unsigned int *>(done + q) = 1u;
         }
         __syncthreads();
     }
@@ -824,7 +840,11 @@ __global__ void __launch_bounds__(kGroupThreads, kGroupMinBlocks) k_query_groups
             if (gtid == 0) atomicAdd(invalid, 1ull);
             continue;
         }
+#ifdef EAT_GROUPS_FLAT
+        grid_solve<SW, kSchedFlat>(ix, w, s, ts, dstv ? nullptr : orow, gtid, gsz, cpg, bar, epoch);
+#else
         grid_solve<SW, kSchedFrontier>(ix, w, s, ts, dstv ? nullptr : orow, gtid, gsz, cpg, bar, epoch);
+#endif
         if (dstv && gtid == 0) orow[0] = ld_cg(w.arr + __ldg(ix.perm + dq));
     }
 }
@@ -848,7 +868,7 @@ cudaError_t launch_cta_one(const DevIndex &ix, const CtaArgs &a, const uint32_t 
     e = cudaMemsetAsync(a.qcounter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     kern<<<unsigned(grid), T, smem, st>>>(ix, a.src, a.ts, a.nq, a.out, a.sweeps, a.qcounter, a.invalid, a.counters,
-                                          a.dst, qlist, qcount, ovf_list, ovf_cnt);
+                                          a.dst, qlist, qcount, ovf_list, ovf_cnt, a.done);
     return cudaGetLastError();
 }
 

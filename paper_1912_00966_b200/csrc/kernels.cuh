@@ -80,6 +80,7 @@ struct CtaArgs {
     const uint32_t *dst = nullptr;  // goal-directed targets or NULL
     uint32_t *ovf_list = nullptr;   // [nq] + 1 count word (ovf_cnt): uint16-pass overflow queries
     uint32_t *ovf_cnt = nullptr;
+    unsigned int *done = nullptr;   // streamed e2e: [nq] finished-row flags (mapped host memory) or NULL
     int threads = 256;              // 1024, 512, 384, 256, 192 or 128
     bool arr16 = false;             // uint16 pass (+ uint32 recompute of overflowing queries)
     uint64_t grid_cap = 0;
