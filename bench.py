@@ -429,8 +429,22 @@ def _batch_roofline(tt, src, ts, dev, stream, args, step_ms, st0):
     the HBM fraction and the ncu-measured DRAM traffic beside it."""
     hbm, hbm_src = _hbm_peak()
     if st0["cta_grid"] == 0:
-        return {"bound": "latency", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None, "traffic": None,
-                "kernel": "k_query_groups", "note": "latency-bound frontier sweeps (DESIGN.md §6)"}
+        # batches on CTA groups (e[] in global memory): no instrumented
+        # variant; the DRAM traffic of the ncu capture against HBM peak
+        traffic, src_ = None, None
+        tp = os.path.join(ROOT, "profiles", "traffic_metro_batch.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                tj = json.load(f)
+            traffic = tj["dram_bytes_per_launch"] * len(src) / tj["queries_per_launch"]
+            src_ = tj["source"]
+        mean_launch_s = (sum(step_ms) / len(step_ms)) / 1e3
+        dram_gbs = traffic / mean_launch_s / 1e9 if traffic else None
+        return {"bound": "hbm", "achieved": dram_gbs, "peak": hbm, "unit": "GB/s",
+                "frac": dram_gbs / hbm if dram_gbs else None, "traffic": traffic, "kernel": "k_query_groups",
+                "achieved_is": "measured DRAM bytes (ncu, scaled to this launch's queries) / mean launch time",
+                "traffic_source": src_, "note": "random 32-byte gathers of a non-L2-resident index: latency-bound "
+                                                "(DESIGN.md §6)"}
     try:
         from paper_1912_00966_b200 import counters
 
@@ -612,8 +626,9 @@ def run_gpu(args):
                        "types": st0["num_types"], "queries_per_step": NQ, "queries_per_gpu": nq,
                        "parallelism": f"query-sharded x{world} (contiguous shards, no collective)",
                        "l2": "flushed (256 MiB write) between timed steps",
-                       "kernel": "cta (batched)" if st0["cta_grid"] > 0 else "grid groups (k_query_groups, frontier)",
-                       "subtrips": args.subtrips, "window_s": 1200 if st0["cta_grid"] > 0 else None,
+                       "kernel": "cta (batched)" if st0["cta_grid"] > 0 else
+                       "CTA groups (k_query_groups, warp-flattened pairs + time window)",
+                       "subtrips": args.subtrips, "window_s": 1200 if st0["cta_grid"] > 0 else 2400,
                        "cta_threads": 256 if st0["cta_grid"] > 0 else None,
                        "shortcuts": st0["num_shortcuts"]},
             "parity": parity, "parity_rows": parity_rows,

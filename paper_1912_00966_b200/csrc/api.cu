@@ -77,6 +77,7 @@ struct eat_handle {
     uint32_t subwarp = 8;
     uint32_t mode = EAT_MODE_REPLICATED;
     uint32_t window = EAT_INF;           // CTA schedule time window (EAT_INF = all active vertices)
+    uint32_t group_window = EAT_INF;     // the same for batches on CTA groups (k_query_groups)
     uint32_t cta_threads = 256;          // CTA-kernel variant (batched queries)
     uint32_t lookup_mode = 0;            // 0 Cluster-AP; NEXT-3 ablations 1 (Connection-type-AP), 2 (linear)
     uint32_t cont_budget = 1;            // grid frontier kernel: continuation hops per frontier vertex
@@ -449,6 +450,12 @@ eat_status run_partitioned(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_
 // EAT_BATCH_GROUPS overrides.
 constexpr uint32_t kBatchGroupsMax = 296;
 
+// Default time window of batches on CTA groups (e[] in global memory): metro
+// 1,024 queries 46.4k q/s at 2400 s vs 43.6k at 1200 s and 38.5k at 600 or
+// 7200 s (profiles/r02_ab_groups_flat_schedule.jsonl).  An explicit
+// eat_build_opts.window_seconds applies to both batch kernels.
+constexpr uint32_t kDefaultGroupWindow = 2400;
+
 // Largest graph whose single queries AUTO runs on the one-CTA kernel.
 constexpr uint32_t kAutoCtaMaxVertices = 2048;
 
@@ -570,6 +577,7 @@ eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
     h->subwarp = sw;
     h->mode = o.mode;
     h->window = o.window_seconds == 0 ? EAT_DEFAULT_WINDOW : o.window_seconds;
+    h->group_window = o.window_seconds == 0 ? kDefaultGroupWindow : o.window_seconds;
     h->cta_threads = o.cta_threads == 0 ? 256u : o.cta_threads;
     if (h->cta_threads != 512 && h->cta_threads != 384 && h->cta_threads != 256 && h->cta_threads != 192 &&
         h->cta_threads != 128)
@@ -943,7 +951,9 @@ eat_status launch_batch_groups(eat_handle *h, const uint32_t *d_sources, const u
         CUDA_TRY(eat::sort_queries_by_source(h->ix, d_sources, nq, sc, st));
         qorder = sc.v1;
     }
-    CUDA_TRY(eat::launch_query_groups(h->ix, h->subwarp == 0 ? 32 : int(h->subwarp), h->bgw.data(), h->d_bgw, groups,
+    eat::DevIndex gix = h->ix;
+    gix.window = h->group_window;
+    CUDA_TRY(eat::launch_query_groups(gix, h->subwarp == 0 ? 32 : int(h->subwarp), h->bgw.data(), h->d_bgw, groups,
                                       d_sources, d_times, nq, d_out, d_qcounter, h->d_invalid, d_dst, qorder, st));
     return EAT_OK;
 }

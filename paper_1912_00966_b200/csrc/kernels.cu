@@ -840,10 +840,16 @@ __global__ void __launch_bounds__(kGroupThreads, kGroupMinBlocks) k_query_groups
             if (gtid == 0) atomicAdd(invalid, 1ull);
             continue;
         }
-#ifdef EAT_GROUPS_FLAT
-        grid_solve<SW, kSchedFlat>(ix, w, s, ts, dstv ? nullptr : orow, gtid, gsz, cpg, bar, epoch);
-#else
+        // warp-flattened (vertex, type) pairs with the time window, as the CTA
+        // kernel: a batch is throughput-bound, and the window cuts the type
+        // evaluations a query needs (metro 1,024 queries: 18.0k -> 43.6k q/s
+        // vs the latency-oriented frontier schedule with continuation,
+        // profiles/r02_ab_groups_flat_schedule.jsonl; EAT_GROUPS_FRONTIER
+        // builds the old schedule for A/B)
+#ifdef EAT_GROUPS_FRONTIER
         grid_solve<SW, kSchedFrontier>(ix, w, s, ts, dstv ? nullptr : orow, gtid, gsz, cpg, bar, epoch);
+#else
+        grid_solve<SW, kSchedFlat>(ix, w, s, ts, dstv ? nullptr : orow, gtid, gsz, cpg, bar, epoch);
 #endif
         if (dstv && gtid == 0) orow[0] = ld_cg(w.arr + __ldg(ix.perm + dq));
     }
