@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             const uint32_t best = TGT ? ar.get(di) : uint32_t(kInf);
             const unsigned long long t_sw0 = COUNT ? clock64() : 0ull;
             // ---- 1. select + compact: active = deferred | new
-            uint32_t dmin = kInf, ndef = 0;
+            uint32_t dmin = kInf, ndef = 0;  // ndef: some vertex stays deferred
             for (uint32_t w = tid; w < W; w += kCtaThreads) {
                 uint32_t word = bmD[w] | bmN[w];
                 if (!word) continue;
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                 if (thr < kInf || (TGT && best < kInf)) {
                     sel = 0;
                     uint32_t rest = word;
-                    while (rest) {
+                    while (rest) {  // (two e[] reads in flight per step: -0.7 %, r02_ab_select_unroll.jsonl)
                         const uint32_t b = __ffs(rest) - 1u;
                         rest &= rest - 1u;
                         const uint32_t a = ar.get(w * 32u + b);
@@ -325,15 +325,18 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     }
                 }
                 bmD[w] = word & ~taken;
-                ndef += __popc(word & ~taken);
+                ndef |= word & ~taken;
             }
             if (COUNT && lane == 0) atomicMax(&s_tw[0], clock64() - t_sw0);
+            // (the select spread over fewer warps is slower -- 4 of 8: -6 %, 2: -15 %,
+            // profiles/r02_ab_select_warps.jsonl: the phase is on the sweep's critical path)
             if (window < kInf) {
                 dmin = __reduce_min_sync(0xFFFFFFFFu, dmin);
                 if (lane == 0 && dmin < kInf) atomicMin(&s_tmin[t_nxt], dmin);
             }
-            ndef = __reduce_add_sync(0xFFFFFFFFu, ndef);
-            if (lane == 0 && ndef) atomicAdd(&s_more[p], ndef);
+            // s_more is a flag: every writer stores the same value (a warp
+            // reduction + atomic per warp measured 0.9 % slower)
+            if (ndef) s_more[p] = 1u;
             __syncthreads();
             if (COUNT && tid == 0) {
                 const unsigned long long now = clock64();
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             // consecutive list entries so that small frontiers still spread
             // over all warps
             const uint32_t g = min(32u, max(1u, (F + kCtaWarps - 1u) / kCtaWarps));
-            uint32_t nimpr = 0, imin = kInf;  // improvements; their minimum feeds the next window base
+            uint32_t imin = kInf;  // minimum improved arrival: feeds the next window base
             for (uint32_t k0 = wid * g; k0 < F; k0 += kCtaWarps * g) {
                 const uint32_t j = k0 + lane;
                 uint32_t x = 0, p0 = 0, nt = 0;
@@ -426,18 +429,17 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                         if (cand < old) {
                             atomicOr(bmN + (tr.v >> 5), 1u << (tr.v & 31u));
                             imin = min(imin, cand);
-                            ++nimpr;
                             if (COUNT) ++c_impr;
                         }
                     }
                 }
             }
             if (COUNT && lane == 0) atomicMax(&s_tw[1], clock64() - t_pr0);
-            nimpr = __reduce_add_sync(0xFFFFFFFFu, nimpr);
-            if (lane == 0 && nimpr) atomicAdd(&s_more[p], nimpr);
-            if (window < kInf) {
-                imin = __reduce_min_sync(0xFFFFFFFFu, imin);
-                if (lane == 0 && imin < kInf) atomicMin(&s_tmin[t_nxt], imin);
+            // imin < INF iff this warp improved something
+            imin = __reduce_min_sync(0xFFFFFFFFu, imin);
+            if (lane == 0 && imin < kInf) {
+                s_more[p] = 1u;
+                if (window < kInf) atomicMin(&s_tmin[t_nxt], imin);
             }
             __syncthreads();
             if (COUNT && tid == 0) {
