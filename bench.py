@@ -459,7 +459,7 @@ def _batch_roofline(tt, src, ts, dev, stream, args, step_ms, st0):
                 tj = json.load(f)
             traffic, ncu_src = tj.get("dram_bytes_per_launch"), tj.get("source")
         return {"bound": "l2", "achieved": achieved, "peak": l2, "unit": "GB/s", "frac": achieved / l2,
-                "traffic": traffic, "kernel": "k_query_cta<0,256,512,0,0>",
+                "traffic": traffic, "kernel": f"k_query_cta<0,{st0['cta_threads']},512,0,0>",
                 "peak_source": "measured in this run: eat_probe_read, 32 MiB L2-resident buffer, 128-bit loads",
                 "algorithmic_bytes_per_launch": cnt["algorithmic_bytes"],
                 "layout_bytes_per_launch": cnt["layout_bytes"],
@@ -629,7 +629,7 @@ def run_gpu(args):
                        "kernel": "cta (batched)" if st0["cta_grid"] > 0 else
                        "CTA groups (k_query_groups, warp-flattened pairs + time window)",
                        "subtrips": args.subtrips, "window_s": 1200 if st0["cta_grid"] > 0 else 2400,
-                       "cta_threads": 256 if st0["cta_grid"] > 0 else None,
+                       "cta_threads": st0["cta_threads"] if st0["cta_grid"] > 0 else None,
                        "shortcuts": st0["num_shortcuts"]},
             "parity": parity, "parity_rows": parity_rows,
             "parity_rule": "device rows == oracle rows (serial CSA on the raw timetable), every stop, bit-exact",

@@ -46,7 +46,7 @@ extern "C" {
 #endif
 
 #define EAT_INF 0x7FFFFFFFu
-#define EAT_ABI_VERSION 3u
+#define EAT_ABI_VERSION 4u
 
 typedef enum eat_status {
     EAT_OK = 0,
@@ -137,8 +137,8 @@ typedef struct eat_build_opts {
                                      e[u] <= min_active(e) + window (others stay active); EAT_INF = every
                                      active vertex (the paper's schedule); 0 -> EAT_DEFAULT_WINDOW.
                                      Results are identical for every value (same fixpoint). */
-    uint32_t cta_threads;         /* batched CTA kernel threads per query: 0 -> 256; 512, 384, 256, 192 or 128
-                                     (occupancy knob, tools/sweep_cta.py) */
+    uint32_t cta_threads;         /* batched CTA kernel threads per query: 0 -> 384; 512, 384, 320, 256, 192 or 128
+                                     (occupancy knob, tools/sweep.py) */
     uint32_t subtrips;            /* sub-trip shortcuts (needs tt->trip): 0 off;
                                      1 = r = round(sqrt(k)) per trip of k connections;
                                      2 = r = round(sqrt(average trip length)); >= 3: r itself;
@@ -282,6 +282,8 @@ typedef struct eat_stats {
     uint64_t cluster_singles;     /* single departures (leftovers) held by the hour-cluster slots read */
     uint64_t fallbacks;           /* lookups answered by the next non-empty cluster */
     uint64_t select_bits;         /* active (deferred or new) vertices examined by the CTA kernel's select phases */
+    uint32_t cta_threads;         /* threads per CTA (= per query in flight) of the batched CTA kernel */
+    uint32_t reserved0;
 } eat_stats;
 
 eat_status eat_get_stats(const eat_handle *h, eat_stats *out);

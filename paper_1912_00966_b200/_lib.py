@@ -73,7 +73,8 @@ class eat_stats(ctypes.Structure):
                 ("cta_grid", ctypes.c_uint32), ("num_devices", ctypes.c_uint32),
                 ("edge_evals", ctypes.c_uint64), ("cluster_runs", ctypes.c_uint64),
                 ("cluster_singles", ctypes.c_uint64), ("fallbacks", ctypes.c_uint64),
-                ("select_bits", ctypes.c_uint64)]
+                ("select_bits", ctypes.c_uint64), ("cta_threads", ctypes.c_uint32),
+                ("reserved0", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

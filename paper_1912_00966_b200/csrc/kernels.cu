@@ -905,6 +905,7 @@ cudaError_t launch_cta_variant(const DevIndex &ix, const CtaArgs &a, cudaStream_
         case 1024: return launch_cta_pair<COUNT, 1024, 2048>(ix, a, st);
         case 512: return launch_cta_pair<COUNT, 512, 2048>(ix, a, st);
         case 384: return launch_cta_pair<COUNT, 384, 512>(ix, a, st);
+        case 320: return launch_cta_pair<COUNT, 320, 512>(ix, a, st);
         case 192: return launch_cta_pair<COUNT, 192, 512>(ix, a, st);
         case 128: return launch_cta_pair<COUNT, 128, 512>(ix, a, st);
         default: return launch_cta_pair<COUNT, 256, 512>(ix, a, st);
@@ -983,6 +984,7 @@ int cta_grid_size_a(uint32_t n, int threads) {
         case 1024: return cta_grid_size_t<1024, 2048, A16>(n);
         case 512: return cta_grid_size_t<512, 2048, A16>(n);
         case 384: return cta_grid_size_t<384, 512, A16>(n);
+        case 320: return cta_grid_size_t<320, 512, A16>(n);
         case 192: return cta_grid_size_t<192, 512, A16>(n);
         case 128: return cta_grid_size_t<128, 512, A16>(n);
         default: return cta_grid_size_t<256, 512, A16>(n);

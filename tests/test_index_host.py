@@ -106,7 +106,7 @@ def test_abi_symbols_exported():
     nm = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
     for name in declared:
         assert re.search(rf"\bT {name}$", nm, re.M), f"{name} not exported by libeat.so"
-    assert _lib.eat_abi_version() == 3
+    assert _lib.eat_abi_version() == 4
 
 
 def test_roundtrip_tiny_and_lookup_every_bound():
