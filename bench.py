@@ -335,7 +335,7 @@ def _latency_legs(args, rank, world, dev, stream, flush, city_tt):
         if cfg == "city":  # warm back-to-back figure of both single-query kernels (round-1 key)
             o1 = torch.empty(tt.num_vertices, dtype=torch.int32, device=dev)
             d["warm_ms"] = {}
-            for kname in ("cta", "frontier"):
+            for kname in ("cta", "frontier", "cluster"):
                 e1 = Engine.from_timetable(tt, device=dev, kernel=kname, subtrips=args.subtrips)
                 for _ in range(3):
                     e1.query_device(*synth.SINGLE_QUERY, o1, stream=stream)

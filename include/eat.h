@@ -85,7 +85,9 @@ enum {
 
 /* eat_build_opts.kernel: relaxation schedule for single queries. */
 enum {
-    EAT_KERNEL_AUTO = 0,          /* single queries: CTA kernel for graphs of <= 2048 stops, else FRONTIER; batches: CTA when e[] fits shared memory */
+    EAT_KERNEL_AUTO = 0,          /* single queries: CTA kernel for graphs of <= 2048 stops, CLUSTER when the
+                                     whole index fits the shared memory of a 16-CTA cluster beside e[] (city
+                                     scale), else FRONTIER; batches: CTA when e[] fits shared memory */
     EAT_KERNEL_FRONTIER = 1,      /* grid-wide persistent kernel, worklist frontier, global arr; requested
                                      explicitly, batches also run this schedule (CTA groups, e[] in global) */
     EAT_KERNEL_FULL_SWEEP = 2,    /* grid-wide persistent kernel, every type every sweep, active bitmap */
@@ -95,8 +97,12 @@ enum {
                                      + inboxes; one grid barrier per exchange round */
     EAT_KERNEL_CONNECTION = 5,    /* ablation (NEXT-3): the paper's Connection-version, a thread per raw
                                      connection every sweep (Algorithm 4) */
-    EAT_KERNEL_BITMAP = 6         /* grid-wide persistent kernel, global arr, active-vertex bitmap scanned
+    EAT_KERNEL_BITMAP = 6,        /* grid-wide persistent kernel, global arr, active-vertex bitmap scanned
                                      by warps (warp per 32-vertex word, lanes over types); no worklist */
+    EAT_KERNEL_CLUSTER = 7        /* one thread-block cluster of cluster_ctas CTAs (one per SM) per query,
+                                     e[] and the frontier bitmaps distributed over the CTAs' shared memory
+                                     (DSMEM: ld / atom.min / red.or on the owner CTA), cluster barriers per
+                                     sweep; the CTA kernel's windowed schedule.  Needs |V| <= ~56k x CTAs */
 };
 
 /* eat_build_opts.mode */
@@ -174,6 +180,8 @@ typedef struct eat_build_opts {
                                      writing its own rows (no communication).  devices[0] is the primary:
                                      every other call (single queries, *_device variants, stats) runs there.
                                      Copied at build; caller may free it after eat_build returns. */
+    uint32_t cluster_ctas;        /* EAT_KERNEL_CLUSTER: CTAs per cluster, 2, 4, 8 or 16 (non-portable);
+                                     0 -> the largest that the device schedules for this graph */
 } eat_build_opts;
 
 #define EAT_CONT_NONE 0xFFFFFFFFu
@@ -283,7 +291,7 @@ typedef struct eat_stats {
     uint64_t fallbacks;           /* lookups answered by the next non-empty cluster */
     uint64_t select_bits;         /* active (deferred or new) vertices examined by the CTA kernel's select phases */
     uint32_t cta_threads;         /* threads per CTA (= per query in flight) of the batched CTA kernel */
-    uint32_t reserved0;
+    uint32_t cluster_ctas;        /* EAT_KERNEL_CLUSTER: CTAs per cluster (0 for other kernels) */
 } eat_stats;
 
 eat_status eat_get_stats(const eat_handle *h, eat_stats *out);

@@ -20,7 +20,8 @@ STATUS_NAMES = ["EAT_OK", "EAT_EINVAL", "EAT_ERANGE", "EAT_ENOMEM", "EAT_ECUDA",
                 "EAT_EUNSUPPORTED", "EAT_ESTATE"]
 
 EAT_RENUMBER = {"auto": 0, "none": 1, "bfs": 2, "morton": 3}
-EAT_KERNEL = {"auto": 0, "frontier": 1, "full_sweep": 2, "cta": 3, "async": 4, "connection": 5, "bitmap": 6}
+EAT_KERNEL = {"auto": 0, "frontier": 1, "full_sweep": 2, "cta": 3, "async": 4, "connection": 5, "bitmap": 6,
+              "cluster": 7}
 EAT_KERNEL_NAMES = {v: k for k, v in EAT_KERNEL.items()}
 EAT_MODE = {"replicated": 0, "edge_partitioned": 1}
 EAT_BUILD_HOST_ONLY = 0x1
@@ -53,7 +54,7 @@ class eat_build_opts(ctypes.Structure):
                 ("arr_bits", ctypes.c_uint32), ("lookup", ctypes.c_uint32), ("cluster_dir", ctypes.c_uint32),
                 ("continuation", ctypes.c_uint32), ("exchange", ctypes.c_uint32),
                 ("local_sweeps", ctypes.c_uint32), ("num_devices", ctypes.c_uint32),
-                ("devices", ctypes.POINTER(ctypes.c_int32))]
+                ("devices", ctypes.POINTER(ctypes.c_int32)), ("cluster_ctas", ctypes.c_uint32)]
 
 
 class eat_stats(ctypes.Structure):
@@ -74,7 +75,7 @@ class eat_stats(ctypes.Structure):
                 ("edge_evals", ctypes.c_uint64), ("cluster_runs", ctypes.c_uint64),
                 ("cluster_singles", ctypes.c_uint64), ("fallbacks", ctypes.c_uint64),
                 ("select_bits", ctypes.c_uint64), ("cta_threads", ctypes.c_uint32),
-                ("reserved0", ctypes.c_uint32)]
+                ("cluster_ctas", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

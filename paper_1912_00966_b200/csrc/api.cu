@@ -131,6 +131,10 @@ struct eat_handle {
     uint64_t done_cap = 0;
     int cta_grid = 0;
     uint32_t single_cta_threads = 1024;  // CTA variant of a lone query: 1024 when it fits, else cta_threads
+    uint32_t cluster_ctas = 0;           // EAT_KERNEL_CLUSTER: CTAs per cluster (resolved at build)
+    int cluster_stage = 0;               // ... index staged in shared memory (cluster.cu STAGE)
+    uint32_t cluster_window = EAT_INF;   // ... schedule window (all active vertices unless set: fastest, r02_cluster_*)
+    uint32_t cluster_tl = 0;             // ... most types owned by one CTA
     bool batch_groups = false;  // batches on k_query_groups even when e[] fits shared memory (kernel FRONTIER)
     eat::SortScratch qsort[3];  // k_query_groups query order by source locality, per overflow/pipeline slot
     bool sort_batches = true;   // EAT_SORT_BATCHES=0 disables (A/B)
@@ -459,6 +463,37 @@ constexpr uint32_t kDefaultGroupWindow = 2400;
 // Largest graph whose single queries AUTO runs on the one-CTA kernel.
 constexpr uint32_t kAutoCtaMaxVertices = 2048;
 
+// Most connection types owned by one CTA of a cs-CTA cluster (bitmap word w
+// of 32 vertices belongs to CTA w mod cs; cluster.cu).
+uint32_t cluster_tl_cap(const eat::HostIndex &hx, uint32_t cs) {
+    const uint32_t n = hx.n, W = (n + 31u) / 32u;
+    std::vector<uint64_t> cnt(cs, 0);
+    for (uint32_t w = 0; w < W; ++w)
+        cnt[w % cs] += hx.type_ptr[std::min(32u * w + 32u, n)] - hx.type_ptr[std::min(32u * w, n)];
+    return uint32_t(std::min<uint64_t>(*std::max_element(cnt.begin(), cnt.end()), 0xFFFFFFFFu));
+}
+
+// EAT_KERNEL_CLUSTER configuration: the largest cluster (or `want` CTAs)
+// the device schedules for this graph, at the deepest index staging that fits
+// beside e[] and at least `min_stage`.  Sets cluster_ctas/stage/tl.
+bool pick_cluster(eat_handle *h, uint32_t want, int min_stage) {
+    const char *env = getenv("EAT_CLUSTER_STAGE");  // A/B knob: highest staging level tried
+    const int max_stage = env ? std::max(0, std::min(2, atoi(env))) : 2;
+    for (uint32_t c = 16; c >= 2; c >>= 1) {
+        if (want && c != want) continue;
+        const uint32_t tl = cluster_tl_cap(h->hx, c);
+        for (int stg = max_stage; stg >= min_stage; --stg)
+            if (eat::cluster_max_active(h->hx.n, int(c), stg, tl) > 0) {
+                h->cluster_ctas = c;
+                h->cluster_stage = stg;
+                h->cluster_tl = tl;
+                return true;
+            }
+    }
+    h->cluster_ctas = 0;
+    return false;
+}
+
 eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     h->cta_grid = eat::cta_grid_size(h->hx.n, int(h->cta_threads), h->arr16);
     // a lone query takes the widest CTA (1024 threads, uint32 e[]) when its
@@ -477,15 +512,24 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     // and the only choice once e[] exceeds shared memory; faster than ASYNC
     // on metro/country).  Batches always use the CTA kernel
     // when e[] fits (throughput).
-    if (k == EAT_KERNEL_AUTO)
-        k = (h->cta_grid > 0 && h->hx.n <= kAutoCtaMaxVertices) ? EAT_KERNEL_CTA : EAT_KERNEL_FRONTIER;
+    if (k == EAT_KERNEL_AUTO) {
+        if (h->cta_grid > 0 && h->hx.n <= kAutoCtaMaxVertices) k = EAT_KERNEL_CTA;
+        // graphs whose whole index (type ranges, headers, cluster bases)
+        // fits on chip beside e[] in a 16-CTA cluster: the cluster kernel
+        // (city 0.45 -> 0.32 ms; metro, staged partially, stays on FRONTIER:
+        // 1.82 vs 1.72 ms, profiles/r02_cluster_*.jsonl)
+        else if (h->mode == EAT_MODE_REPLICATED && pick_cluster(h, 16, 2)) k = EAT_KERNEL_CLUSTER;
+        else k = EAT_KERNEL_FRONTIER;
+    }
     else if (k == EAT_KERNEL_FRONTIER)
         h->batch_groups = true;  // explicit FRONTIER: batches use its schedule too (grouped grid kernel)
     if (k == EAT_KERNEL_CTA && (h->cta_grid == 0 || eat::cta_grid_size(h->hx.n, int(h->single_cta_threads), false) == 0))
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
     if (k == EAT_KERNEL_ASYNC && !async_ok)
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_ASYNC: a 1/SM-count slice of the arrival array does not fit shared memory");
-    if (k > EAT_KERNEL_BITMAP) return fail(EAT_EINVAL, "unknown kernel");
+    if (k > EAT_KERNEL_CLUSTER) return fail(EAT_EINVAL, "unknown kernel");
+    if (k == EAT_KERNEL_CLUSTER && !pick_cluster(h, h->cluster_ctas, 0))
+        return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CLUSTER: e[] does not fit the shared memory of a schedulable cluster");
     if (k == EAT_KERNEL_CONNECTION) {  // raw connections on the device (ablation schedule)
         CUDA_TRY(cudaMalloc(&h->d_conns, std::max<size_t>(h->raw.size(), 1) * sizeof(uint4)));
         CUDA_TRY(cudaMemcpy(h->d_conns, h->raw.data(), h->raw.size() * sizeof(uint4), cudaMemcpyHostToDevice));
@@ -534,6 +578,24 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
         a.arr16 = false;
         a.grid_cap = 1;
         CUDA_TRY(eat::launch_query_cta(h->ix, a, st));
+    } else if (h->kernel == EAT_KERNEL_CLUSTER) {
+        uint32_t q[2] = {s, t_s};
+        CUDA_TRY(cudaMemcpyAsync(h->d_q1, q, sizeof(q), cudaMemcpyHostToDevice, st));
+        eat::ClusterArgs a;
+        a.src = h->d_q1;
+        a.ts = h->d_q1 + 1;
+        a.nq = 1;
+        a.out = d_out;
+        a.sweeps = h->d_sweeps1;
+        a.qcounter = h->d_counter;
+        a.invalid = h->d_invalid;
+        a.cs = int(h->cluster_ctas);
+        a.stage = h->cluster_stage;
+        a.tl_cap = h->cluster_tl;
+        a.max_clusters = 1;
+        eat::DevIndex cix = h->ix;
+        cix.window = h->cluster_window;
+        CUDA_TRY(eat::launch_query_cluster(cix, a, st));
     } else if (h->kernel == EAT_KERNEL_ASYNC) {
         CUDA_TRY(eat::launch_query_async(h->ix, h->aw, s, t_s, d_out, st));
         CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->aw.ctl + 9, 4, cudaMemcpyDeviceToDevice, st));
@@ -569,7 +631,7 @@ eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
     if (sw != 0 && sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
         return fail(EAT_EINVAL, "subwarp must be 0 (default 32), 1, 2, 4, 8, 16, 32 or 64 (flattened pairs)");
     if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
-    if (o.kernel > EAT_KERNEL_BITMAP) return fail(EAT_EINVAL, "unknown kernel");
+    if (o.kernel > EAT_KERNEL_CLUSTER) return fail(EAT_EINVAL, "unknown kernel");
     if (o.lookup > 2) return fail(EAT_EINVAL, "lookup must be 0 (Cluster-AP), 1 (Connection-type-AP) or 2 (linear)");
     const uint32_t pc = o.part_count ? o.part_count : 1;
     if (o.mode == EAT_MODE_EDGE_PARTITIONED && o.part_rank >= pc)
@@ -578,6 +640,7 @@ eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
     h->mode = o.mode;
     h->window = o.window_seconds == 0 ? EAT_DEFAULT_WINDOW : o.window_seconds;
     h->group_window = o.window_seconds == 0 ? kDefaultGroupWindow : o.window_seconds;
+    h->cluster_window = o.window_seconds == 0 ? EAT_INF : o.window_seconds;
     h->cta_threads = o.cta_threads == 0 ? 384u : o.cta_threads;
     if (h->cta_threads != 512 && h->cta_threads != 384 && h->cta_threads != 320 && h->cta_threads != 256 &&
         h->cta_threads != 192 && h->cta_threads != 128)
@@ -597,6 +660,9 @@ eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
     if (o.local_sweeps && (o.mode != EAT_MODE_EDGE_PARTITIONED || o.exchange != EAT_EXCHANGE_ALLREDUCE))
         return fail(EAT_EINVAL, "local_sweeps applies to EDGE_PARTITIONED handles with EAT_EXCHANGE_ALLREDUCE");
     h->local_sweeps = o.local_sweeps;
+    if (o.cluster_ctas && (o.cluster_ctas < 2 || o.cluster_ctas > 16 || (o.cluster_ctas & (o.cluster_ctas - 1))))
+        return fail(EAT_EINVAL, "cluster_ctas must be 2, 4, 8 or 16");
+    h->cluster_ctas = o.cluster_ctas;
     // all partitions in this process (one device) unless this is one rank of
     // several processes (NCCL id given, or EAT_BUILD_MULTIPROCESS for PEER)
     h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 &&
@@ -788,6 +854,7 @@ eat_status eat_get_stats(const eat_handle *hc, eat_stats *out) {
         h->st.invalid_queries = inv;
         h->st.cta_grid = uint32_t(h->cta_grid);
         h->st.cta_threads = h->cta_threads;
+        h->st.cluster_ctas = h->kernel == EAT_KERNEL_CLUSTER ? h->cluster_ctas : 0u;
         if (h->kernel == EAT_KERNEL_ASYNC && h->mode != EAT_MODE_EDGE_PARTITIONED) {
             uint32_t rr = 0;
             CUDA_TRY(cudaMemcpy(&rr, h->d_rounds1, 4, cudaMemcpyDeviceToHost));

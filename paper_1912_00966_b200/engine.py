@@ -68,7 +68,7 @@ class Engine:
                  cta_threads: int = 0, subtrips: int = 0, trip=None, arr_bits: int = 0,
                  cluster_dir: str = "auto", lookup: str = "cluster_ap", continuation: Optional[int] = None,
                  exchange: str = "allreduce", multiprocess: bool = False, local_sweeps: int = 0,
-                 devices=None):
+                 devices=None, cluster_ctas: int = 0):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
@@ -103,7 +103,7 @@ class Engine:
                                    exchange=_lib.EAT_EXCHANGE[exchange], local_sweeps=int(local_sweeps),
                                    num_devices=len(self._devs) if self._devs is not None else 0,
                                    devices=ctypes.cast(self._devs, ctypes.POINTER(ctypes.c_int32))
-                                   if self._devs is not None else None)
+                                   if self._devs is not None else None, cluster_ctas=int(cluster_ctas))
         self._h = _lib.eat_build(tt, opts)
         self.device = -1 if host_only else int(device)
         if self.device < 0 and not host_only:

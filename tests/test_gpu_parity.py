@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_1912_00966_b200 import Engine, EatError, _lib  # noqa: E402
 
-KERNELS = ["cta", "frontier", "full_sweep", "async", "bitmap"]
+KERNELS = ["cta", "frontier", "full_sweep", "async", "bitmap", "cluster"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -110,7 +110,9 @@ def test_random_small_instances(kernel):
                                     subwarp=[1, 2, 4, 8, 16, 32, 0, 64][seed % 8],
                                     cta_threads=[256, 384, 512, 192, 128][seed % 5], arr_bits=[16, 32][seed % 2],
                                     cluster_dir=["auto", "dense", "compact"][seed % 3],
-                                    continuation=[None, 0, 2, 4, 64, 1, 16][seed % 7])
+                                    continuation=[None, 0, 2, 4, 64, 1, 16][seed % 7],
+                                    cluster_ctas=[0, 2, 4, 8, 16, 16][seed % 6],
+                                    window=[0, 60, 0x7FFFFFFF][seed % 3] if kernel == "cluster" else 0)
         csa = oracle.CSA(tt.num_vertices, *tt.arrays())
         rng = np.random.default_rng(seed)
         for _ in range(3):
@@ -228,14 +230,32 @@ def test_metro_single_query():
     """BASELINE configs[3]: metro network, global e[] (frontier kernel)."""
     tt = synth.generate("metro")
     eng = Engine.from_timetable(tt)
-    assert eng.stats()["kernel_name"] in ("frontier", "cta", "async")
+    assert eng.stats()["kernel_name"] in ("frontier", "cta", "async", "cluster")
     csa = oracle.CSA(tt.num_vertices, *tt.arrays())
     for s, t_s in [synth.SINGLE_QUERY, (777, 30000)]:
         _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"metro ({s},{t_s})")
-    for kernel in ("frontier", "async"):
+    for kernel in ("frontier", "async", "cluster"):
         e2 = Engine.from_timetable(tt, kernel=kernel)
         for s, t_s in [synth.SINGLE_QUERY, (91, 50000)]:
             _assert_rows(e2.query(s, t_s), csa.query(s, t_s), f"metro {kernel} ({s},{t_s})")
+
+
+@pytest.mark.parametrize("ctas", [2, 4, 8, 16])
+def test_cluster_kernel_sizes(ctas):
+    """EAT_KERNEL_CLUSTER with every cluster size: e[] spread over 2..16
+    CTAs' shared memory (DSMEM), tiny + city queries incl. invalid-free
+    repeats on one handle, sub-trips r = 3."""
+    for name in ("tiny", "city"):
+        tt = synth.generate(name)
+        csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+        eng = Engine.from_timetable(tt, kernel="cluster", cluster_ctas=ctas, subtrips=3)
+        st = eng.stats()
+        assert st["kernel_name"] == "cluster" and st["cluster_ctas"] == ctas
+        rng = np.random.default_rng(ctas)
+        qs = [synth.SINGLE_QUERY] + [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 86400))) for _ in range(6)]
+        for s, t_s in qs:
+            _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"{name} cluster{ctas} ({s},{t_s})")
+        eng.close()
 
 
 def test_metro_batched_groups():
