@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
             }
         }
     };
+    cl_sync();  // every CTA of the cluster has started (DSMEM may be touched only after this)
     fetch_query();
     cl_sync();
     for (;;) {

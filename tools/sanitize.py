@@ -27,6 +27,11 @@ CASES = {
     "cta_batch16": ("k_query_cta (uint16 e[] pass + uint32 recompute)", dict(arr_bits=16), "batch"),
     "cta_batch32": ("k_query_cta (uint32 e[])", dict(arr_bits=32), "batch"),
     "cta_targets": ("k_query_cta<TGT> (goal-directed)", dict(), "targets"),
+    "cta_batch384": ("k_query_cta (384 threads, uint32 e[]: the batch default)", dict(cta_threads=384, arr_bits=32),
+                     "batch"),
+    "cluster16": ("k_query_cluster<2> (16 CTAs, DSMEM e[], staged index)", dict(kernel="cluster", cluster_ctas=16),
+                  "single"),
+    "cluster2": ("k_query_cluster (2 CTAs)", dict(kernel="cluster", cluster_ctas=2, window=600), "single"),
     "grid_frontier": ("k_query_grid<32, frontier>", dict(kernel="frontier"), "single"),
     "grid_flat": ("k_query_grid<32, flat> (subwarp 64)", dict(kernel="frontier", subwarp=64), "single"),
     "grid_full": ("k_query_grid<1, full sweep>", dict(kernel="full_sweep"), "single"),
