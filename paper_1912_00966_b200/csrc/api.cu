@@ -1028,6 +1028,9 @@ eat_status launch_batch_groups(eat_handle *h, const uint32_t *d_sources, const u
 
 eat_status enqueue_batch(eat_handle *h, const uint32_t *d_sources, const uint32_t *d_times, uint64_t nq,
                          uint32_t *d_out, cudaStream_t st, unsigned long long *d_qcounter, int slot = 0) {
+    // (batches on the cluster kernel, one query per 2/4/8-CTA cluster: metro
+    // 1,024 queries 38.7k / 23.8k / 12.8k q/s vs 46.1k on k_query_groups --
+    // profiles/r02_ab_metro_batch_cluster.jsonl; not used)
     if (h->cta_grid > 0 && !h->batch_groups) return launch_batch_cta(h, d_sources, d_times, nq, d_out, st, d_qcounter, slot, nullptr);
     return launch_batch_groups(h, d_sources, d_times, nq, d_out, st, d_qcounter, nullptr, slot);
 }
