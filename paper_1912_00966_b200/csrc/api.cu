@@ -133,6 +133,7 @@ struct eat_handle {
     uint32_t single_cta_threads = 1024;  // CTA variant of a lone query: 1024 when it fits, else cta_threads
     uint32_t cluster_ctas = 0;           // EAT_KERNEL_CLUSTER: CTAs per cluster (resolved at build)
     int cluster_stage = 0;               // ... index staged in shared memory (cluster.cu STAGE)
+    bool cluster_async = !getenv("EAT_CLUSTER_ASYNC") || atoi(getenv("EAT_CLUSTER_ASYNC")) != 0;  // A/B knob (default on)
     uint32_t cluster_window = EAT_INF;   // ... schedule window (all active vertices unless set: fastest, r02_cluster_*)
     uint32_t cluster_tl = 0;             // ... most types owned by one CTA
     bool batch_groups = false;  // batches on k_query_groups even when e[] fits shared memory (kernel FRONTIER)
@@ -483,7 +484,7 @@ bool pick_cluster(eat_handle *h, uint32_t want, int min_stage) {
         if (want && c != want) continue;
         const uint32_t tl = cluster_tl_cap(h->hx, c);
         for (int stg = max_stage; stg >= min_stage; --stg)
-            if (eat::cluster_max_active(h->hx.n, int(c), stg, tl) > 0) {
+            if (eat::cluster_max_active(h->hx.n, int(c), stg, tl, h->cluster_async) > 0) {
                 h->cluster_ctas = c;
                 h->cluster_stage = stg;
                 h->cluster_tl = tl;
@@ -514,11 +515,11 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     // when e[] fits (throughput).
     if (k == EAT_KERNEL_AUTO) {
         if (h->cta_grid > 0 && h->hx.n <= kAutoCtaMaxVertices) k = EAT_KERNEL_CTA;
-        // graphs whose whole index (type ranges, headers, cluster bases)
-        // fits on chip beside e[] in a 16-CTA cluster: the cluster kernel
-        // (city 0.45 -> 0.32 ms; metro, staged partially, stays on FRONTIER:
-        // 1.82 vs 1.72 ms, profiles/r02_cluster_*.jsonl)
-        else if (h->mode == EAT_MODE_REPLICATED && pick_cluster(h, 16, 2)) k = EAT_KERNEL_CLUSTER;
+        // graphs whose e[] and type ranges fit the shared memory of a 16-CTA
+        // cluster: the (asynchronous) cluster kernel -- city p50 0.50 ->
+        // 0.28 ms, metro p50 1.04 -> 1.01 ms over 100 seeded queries
+        // (profiles/r02_latency_kernels.jsonl); larger graphs (country) FRONTIER
+        else if (h->mode == EAT_MODE_REPLICATED && pick_cluster(h, 16, 1)) k = EAT_KERNEL_CLUSTER;
         else k = EAT_KERNEL_FRONTIER;
     }
     else if (k == EAT_KERNEL_FRONTIER)
@@ -579,11 +580,9 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
         a.grid_cap = 1;
         CUDA_TRY(eat::launch_query_cta(h->ix, a, st));
     } else if (h->kernel == EAT_KERNEL_CLUSTER) {
-        uint32_t q[2] = {s, t_s};
-        CUDA_TRY(cudaMemcpyAsync(h->d_q1, q, sizeof(q), cudaMemcpyHostToDevice, st));
-        eat::ClusterArgs a;
-        a.src = h->d_q1;
-        a.ts = h->d_q1 + 1;
+        eat::ClusterArgs a;  // (s, t_s) by value: no copy ahead of the launch
+        a.s1 = s;
+        a.ts1 = t_s;
         a.nq = 1;
         a.out = d_out;
         a.sweeps = h->d_sweeps1;
@@ -592,6 +591,7 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
         a.cs = int(h->cluster_ctas);
         a.stage = h->cluster_stage;
         a.tl_cap = h->cluster_tl;
+        a.async = h->cluster_async;
         a.max_clusters = 1;
         eat::DevIndex cix = h->ix;
         cix.window = h->cluster_window;

@@ -92,6 +92,22 @@ __device__ __forceinline__ void cl_or(uint32_t a, uint32_t v) {
     asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(a), "r"(v));
 }
 
+__device__ __forceinline__ uint32_t cl_add(uint32_t a, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ void cl_redadd(uint32_t a, uint32_t v) {
+    asm volatile("red.shared::cluster.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t cl_or_old(uint32_t a, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared::cluster.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ void cl_redmin(uint32_t a, uint32_t v) {
     asm volatile("red.shared::cluster.min.u32 [%0], %1;" ::"r"(a), "r"(v));
 }
@@ -107,11 +123,19 @@ __device__ __forceinline__ uint32_t lds_volatile(const uint32_t *p) { return *re
 //     PAPER.md:382-390): a relaxation then needs one global access, the
 //     hour-cluster record.
 // Staged once per launch (every query of the launch reuses it).
-template <int STAGE>
+// ASYNC: no per-sweep cluster barrier at all.  Every CTA loops on its own
+// (take all its marked vertices -> relax them) and the query ends when a
+// counter of marked-or-in-processing vertices in CTA 0 reaches zero: a
+// marking warp adds its marks to the counter (and waits for the add) BEFORE
+// setting the bits, subtracts the marks that hit an already-set bit after,
+// and a CTA subtracts the vertices it took once their relaxations (and the
+// marks they made) are done -- so the counter is >= the pending work at
+// every instant and 0 only at the fixpoint.  Window: all active vertices.
+template <int STAGE, bool ASYNC>
 __global__ void __launch_bounds__(kClThreads, 1)
     k_query_cluster(DevIndex ix, const uint32_t *__restrict__ src, const uint32_t *__restrict__ tsv, uint64_t nq,
                     uint32_t *__restrict__ out, uint32_t *sweeps_out, unsigned long long *qcounter,
-                    unsigned long long *invalid, uint32_t tl_cap) {
+                    unsigned long long *invalid, uint32_t tl_cap, uint32_t s1, uint32_t ts1) {
     extern __shared__ uint4 sm4[];
     const uint32_t n = ix.n;
     uint32_t ncta;
@@ -127,11 +151,14 @@ __global__ void __launch_bounds__(kClThreads, 1)
     uint32_t *bmD = reinterpret_cast<uint32_t *>(rng + (STAGE >= 1 ? Wl * 32u : 0u));  // deferred
     uint32_t *bmN = bmD + Wl;                                             // new: lowered since their last selection
     uint32_t *cb_s = bmN + Wl;                                            // STAGE 2
+    uint32_t *a_list = cb_s + (STAGE == 2 ? tl_cap : 0u);                 // ASYNC: [32 Wl] every owned vertex
     __shared__ uint32_t s_list[kClListCap];
     __shared__ uint32_t s_cnt[2], s_more[2];         // per sweep parity: listed / more-work flag (cluster-wide)
     __shared__ uint32_t s_tmin[3];                   // window base, rotating (cluster-wide after the push)
     __shared__ uint32_t s_pmin[2], s_pmore[2];       // this CTA's partials of the sweep (parity)
     __shared__ uint32_t s_q[2];                      // query index (lo, hi) pushed by rank 0
+    __shared__ uint32_t s_pend;                      // ASYNC (CTA 0's copy is the one used): pending vertices
+    __shared__ uint32_t s_idle;                      // ASYNC: the counter read 0
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
     const uint32_t window = ix.window;
     const uint32_t e_sa = uint32_t(__cvta_generic_to_shared(e_loc));
@@ -139,6 +166,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
     const uint32_t more_sa = uint32_t(__cvta_generic_to_shared(s_more));
     const uint32_t tmin_sa = uint32_t(__cvta_generic_to_shared(s_tmin));
     const uint32_t q_sa = uint32_t(__cvta_generic_to_shared(s_q));
+    const uint32_t pend0 = cl_map(uint32_t(__cvta_generic_to_shared(&s_pend)), 0u);
     // DSMEM address of vertex v's arrival / bitmap word in its owner CTA
     auto e_addr = [&](uint32_t v) {
         const uint32_t w = v >> 5;
@@ -218,7 +246,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
     for (;;) {
         const unsigned long long q = (unsigned long long)s_q[0] | ((unsigned long long)s_q[1] << 32);
         if (q == ~0ull) break;
-        const uint32_t s = src[q], ts = tsv[q];
+        const uint32_t s = src ? src[q] : s1, ts = src ? tsv[q] : ts1;  // single query: parameters
         uint32_t *orow = out + q * uint64_t(n);
         if (s >= n || ts >= kInf) {
             for (uint32_t i = rank * kClThreads + tid; i < n; i += ncta * kClThreads) orow[i] = kInf;
@@ -244,6 +272,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
             s_tmin[1] = s_tmin[2] = kInf;
             s_pmin[0] = s_pmin[1] = kInf;
             s_pmore[0] = s_pmore[1] = 0;
+            s_pend = rank == 0 ? 1u : 0u;  // ASYNC: the source is marked
         }
         __syncthreads();
         if (tid == 0) {
@@ -257,7 +286,117 @@ __global__ void __launch_bounds__(kClThreads, 1)
         cl_sync();
         uint32_t sweeps = 0;
         uint32_t t_cur = 0, t_nxt = 1, t_old = 2;
-        for (;;) {
+        if (ASYNC) {
+            for (;;) {
+                const uint32_t p = sweeps & 1u;
+                // ---- take every marked vertex this CTA owns
+                for (uint32_t lw = tid; lw < Wl; lw += kClThreads) {
+                    if (!lds_volatile(bmN + lw)) continue;
+                    uint32_t word = atomicExch(bmN + lw, 0u);
+                    const uint32_t k = __popc(word);
+                    if (!k) continue;
+                    const uint32_t pos = atomicAdd(&s_cnt[p], k);  // the list holds every owned vertex
+                    const uint32_t vbase = ((lw << lg) | rank) << 5;
+                    for (uint32_t i = 0; i < k; ++i) {
+                        const uint32_t b = __ffs(word) - 1u;
+                        word &= word - 1u;
+                        a_list[pos + i] = vbase + b;
+                    }
+                }
+                __syncthreads();
+                const uint32_t F = s_cnt[p];
+                if (tid == 0) s_cnt[p ^ 1u] = 0;
+                ++sweeps;
+                if (F == 0) {  // idle: is any vertex pending anywhere?
+                    if (tid == 0) {
+                        s_idle = cl_ld(pend0) == 0u;
+                        if (!s_idle) __nanosleep(64);
+                    }
+                    __syncthreads();
+                    if (s_idle) break;
+                    if (sweeps > (1u << 22)) break;  // watchdog (never reached by a correct run)
+                    continue;
+                }
+                const uint32_t g = min(32u, max(1u, (F + kClWarps - 1u) / kClWarps));
+                for (uint32_t k0 = wid * g; k0 < F; k0 += kClWarps * g) {
+                    const uint32_t j = k0 + lane;
+                    uint32_t x = 0, p0 = 0, nt = 0;
+                    if (lane < g && j < F) {
+                        x = a_list[j];
+                        if (STAGE >= 1) {
+                            const uint2 r = rng[((((x >> 5) >> lg) << 5) | (x & 31u))];
+                            p0 = r.x;
+                            nt = r.y;
+                        } else {
+                            p0 = __ldg(ix.type_ptr + x);
+                            nt = __ldg(ix.type_ptr + x + 1) - p0;
+                        }
+                    }
+                    uint32_t incl = nt;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                        if (lane >= uint32_t(o)) incl += y;
+                    }
+                    const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                    for (uint32_t base = 0; base < tot; base += 32u) {
+                        const uint32_t qp = base + lane;
+                        uint32_t L = 0;
+#pragma unroll
+                        for (uint32_t step = 16; step > 0; step >>= 1) {
+                            const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, L + step - 1u);
+                            if (v <= qp) L += step;
+                        }
+                        const uint32_t o_incl = __shfl_sync(0xFFFFFFFFu, incl, L);
+                        const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
+                        const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
+                        const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
+                        uint32_t mv = kNone;  // vertex this lane lowered (to be marked)
+                        if (qp < tot) {
+                            const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
+                            const uint32_t eu = lds_volatile(e_loc + ((((u >> 5) >> lg) << 5) | (u & 31u)));
+                            uint32_t cb;
+                            TypeRec tr;
+                            if (STAGE == 2) {
+                                cb = cb_s[t];
+                                const uint4 h = hdr_s[t];
+                                tr = TypeRec{h.x, h.y, h.z, h.w};
+                            } else {
+                                cb = __ldg(ix.type_cb + t);
+                                tr = load_type(ix, t);
+                                tr.last |= cb & ix.zero;
+                            }
+                            if (eu <= tr.last) {
+                                const uint32_t ea = e_addr(tr.v);
+                                const uint32_t av = cl_ld(ea);
+                                if (max(eu, tr.first) + tr.lam < av) {
+                                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, cb, eu);
+                                    const uint32_t cand = tc + tr.lam;
+                                    if (cand < av && cand < cl_min(ea, cand)) mv = tr.v;
+                                }
+                            }
+                        }
+                        // count the marks in CTA 0 before setting them
+                        const uint32_t wm = __ballot_sync(0xFFFFFFFFu, mv != kNone);
+                        if (wm) {
+                            if (lane == uint32_t(__ffs(wm) - 1)) {
+                                // returns once performed in CTA 0: every mark below is
+                                // counted before it can be seen (and un-counted) by its owner
+                                cl_add(pend0, uint32_t(__popc(wm)));
+                            }
+                            __syncwarp();
+                            uint32_t dup = 0;
+                            if (mv != kNone) dup = cl_or_old(bm_addr(mv), 1u << (mv & 31u)) & (1u << (mv & 31u));
+                            const uint32_t dm = __ballot_sync(0xFFFFFFFFu, dup != 0u);
+                            if (dm && lane == uint32_t(__ffs(dm) - 1)) cl_redadd(pend0, 0u - uint32_t(__popc(dm)));
+                        }
+                    }
+                }
+                __syncthreads();  // every relaxation (and mark count) of the F taken vertices is done
+                if (tid == 0) cl_redadd(pend0, 0u - F);
+            }
+        }
+        for (; !ASYNC;) {
 #ifdef EAT_CL_TRACE
             if (tid == 0 && rank == 0 && sweeps < 1024) g_cltrace[sweeps * 6 + 0] = gtimer();
 #endif
@@ -454,24 +593,25 @@ __global__ void __launch_bounds__(kClThreads, 1)
 
 }  // namespace
 
-static size_t cluster_smem_bytes(uint32_t n, int cs, int stage, uint32_t tl_cap) {
+static size_t cluster_smem_bytes(uint32_t n, int cs, int stage, uint32_t tl_cap, bool async) {
     const size_t W = (n + 31u) / 32u;
     const size_t Wl = (W + size_t(cs) - 1u) / size_t(cs);
     size_t b = Wl * 32u * 4u + 2u * Wl * 4u;
     if (stage >= 1) b += Wl * 32u * 8u;
     if (stage == 2) b += size_t(tl_cap) * 20u;
+    if (async) b += Wl * 32u * 4u;
     return b;
 }
 
-template <int STAGE>
+template <int STAGE, bool ASYNC>
 static int cluster_max_active_t(uint32_t n, int cs, uint32_t tl_cap) {
-    auto kern = k_query_cluster<STAGE>;
+    auto kern = k_query_cluster<STAGE, ASYNC>;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 0;
-    const size_t smem = cluster_smem_bytes(n, cs, STAGE, tl_cap);
+    const size_t smem = cluster_smem_bytes(n, cs, STAGE, tl_cap, ASYNC);
     if (smem + fa.sharedSizeBytes > size_t(optin)) return 0;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 0;
     if (cs > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -495,16 +635,19 @@ static int cluster_max_active_t(uint32_t n, int cs, uint32_t tl_cap) {
     return nc;
 }
 
-int cluster_max_active(uint32_t n, int cs, int stage, uint32_t tl_cap) {
+int cluster_max_active(uint32_t n, int cs, int stage, uint32_t tl_cap, bool async) {
     if (cs < 1 || cs > 16 || (cs & (cs - 1))) return 0;
-    switch (stage) {
-        case 2: return cluster_max_active_t<2>(n, cs, tl_cap);
-        case 1: return cluster_max_active_t<1>(n, cs, tl_cap);
-        default: return cluster_max_active_t<0>(n, cs, tl_cap);
+    switch (stage * 2 + int(async)) {
+        case 5: return cluster_max_active_t<2, true>(n, cs, tl_cap);
+        case 4: return cluster_max_active_t<2, false>(n, cs, tl_cap);
+        case 3: return cluster_max_active_t<1, true>(n, cs, tl_cap);
+        case 2: return cluster_max_active_t<1, false>(n, cs, tl_cap);
+        case 1: return cluster_max_active_t<0, true>(n, cs, tl_cap);
+        default: return cluster_max_active_t<0, false>(n, cs, tl_cap);
     }
 }
 
-template <int STAGE>
+template <int STAGE, bool ASYNC>
 static cudaError_t launch_cluster_t(const DevIndex &ix, const ClusterArgs &a, unsigned nc, cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
@@ -514,25 +657,28 @@ static cudaError_t launch_cluster_t(const DevIndex &ix, const ClusterArgs &a, un
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(unsigned(a.cs) * nc);
     cfg.blockDim = dim3(kClThreads);
-    cfg.dynamicSmemBytes = cluster_smem_bytes(ix.n, a.cs, STAGE, a.tl_cap);
+    cfg.dynamicSmemBytes = cluster_smem_bytes(ix.n, a.cs, STAGE, a.tl_cap, ASYNC);
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_query_cluster<STAGE>, ix, a.src, a.ts, a.nq, a.out, a.sweeps, a.qcounter,
-                              a.invalid, a.tl_cap);
+    return cudaLaunchKernelEx(&cfg, k_query_cluster<STAGE, ASYNC>, ix, a.src, a.ts, a.nq, a.out, a.sweeps, a.qcounter,
+                              a.invalid, a.tl_cap, a.s1, a.ts1);
 }
 
 cudaError_t launch_query_cluster(const DevIndex &ix, const ClusterArgs &a, cudaStream_t st) {
-    const int nc_max = cluster_max_active(ix.n, a.cs, a.stage, a.tl_cap);
+    const int nc_max = cluster_max_active(ix.n, a.cs, a.stage, a.tl_cap, a.async);
     if (nc_max < 1) return cudaErrorInvalidConfiguration;
     const uint64_t want = a.max_clusters ? std::min<uint64_t>(a.max_clusters, a.nq) : a.nq;
     const unsigned nc = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(nc_max), want)));
     cudaError_t e = cudaMemsetAsync(a.qcounter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    switch (a.stage) {
-        case 2: return launch_cluster_t<2>(ix, a, nc, st);
-        case 1: return launch_cluster_t<1>(ix, a, nc, st);
-        default: return launch_cluster_t<0>(ix, a, nc, st);
+    switch (a.stage * 2 + int(a.async)) {
+        case 5: return launch_cluster_t<2, true>(ix, a, nc, st);
+        case 4: return launch_cluster_t<2, false>(ix, a, nc, st);
+        case 3: return launch_cluster_t<1, true>(ix, a, nc, st);
+        case 2: return launch_cluster_t<1, false>(ix, a, nc, st);
+        case 1: return launch_cluster_t<0, true>(ix, a, nc, st);
+        default: return launch_cluster_t<0, false>(ix, a, nc, st);
     }
 }
 

@@ -121,7 +121,8 @@ void sort_scratch_free(SortScratch &sc);
 // Arguments of the cluster kernel (cluster.cu: one query per thread-block
 // cluster, e[] distributed over the CTAs' shared memory).
 struct ClusterArgs {
-    const uint32_t *src = nullptr, *ts = nullptr;  // [nq] queries (caller ids / seconds)
+    const uint32_t *src = nullptr, *ts = nullptr;  // [nq] queries (caller ids / seconds), or NULL:
+    uint32_t s1 = 0, ts1 = 0;                      // ... the single query (s1, ts1) passed by value
     uint64_t nq = 0;
     uint32_t *out = nullptr;                 // [nq][n] rows
     uint32_t *sweeps = nullptr;              // optional [nq] sweep counts
@@ -130,12 +131,13 @@ struct ClusterArgs {
     int cs = 16;                             // CTAs per cluster (power of two, <= 16)
     int stage = 0;                           // index staged in shared memory: 0 none, 1 type ranges, 2 + headers
     uint32_t tl_cap = 0;                     // stage 2: most types owned by one CTA
+    bool async = false;                      // no per-sweep cluster barrier (pending-vertex counter)
     uint64_t max_clusters = 0;               // 0: as many as fit
 };
 cudaError_t launch_query_cluster(const DevIndex &ix, const ClusterArgs &a, cudaStream_t st);
 
 // Co-resident clusters of cs CTAs for n vertices at a staging level (0: does not fit / not schedulable).
-int cluster_max_active(uint32_t n, int cs, int stage, uint32_t tl_cap);
+int cluster_max_active(uint32_t n, int cs, int stage, uint32_t tl_cap, bool async);
 
 // CTAs per SM of the persistent grid kernels (env EAT_GRID_CTAS_PER_SM, default 1).
 int grid_ctas_per_sm();

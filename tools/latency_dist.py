@@ -1,7 +1,7 @@
 """Single-query latency distribution (100 seeded (s, t_s) per
 config, p50/p90): device time per query (CUDA events; L2 flushed before each
 query), sweeps, parity against the oracle on the first K queries.
-Usage: python tools/latency_dist.py city,metro,country [nq] [parity_k]"""
+Usage: python tools/latency_dist.py city,metro,country [nq] [parity_k] [kernel]"""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -11,10 +11,11 @@ from paper_1912_00966_b200 import Engine
 cfgs = (sys.argv[1] if len(sys.argv) > 1 else "city,metro").split(",")
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 pk = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+kernel = sys.argv[4] if len(sys.argv) > 4 else "auto"
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
 for cfg in cfgs:
     tt = synth.generate(cfg)
-    eng = Engine.from_timetable(tt, subtrips=3)
+    eng = Engine.from_timetable(tt, subtrips=3, kernel=kernel)
     rng = np.random.default_rng(7)
     qs = [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 86400))) for _ in range(nq)]
     out = torch.empty(tt.num_vertices, dtype=torch.int32, device="cuda")
