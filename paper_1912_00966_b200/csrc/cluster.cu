@@ -112,6 +112,16 @@ __device__ __forceinline__ void cl_redmin(uint32_t a, uint32_t v) {
     asm volatile("red.shared::cluster.min.u32 [%0], %1;" ::"r"(a), "r"(v));
 }
 
+// 32-byte cluster record r, as volatile loads (issued where written, not
+// sunk into the branch that consumes them)
+__device__ __forceinline__ void ldg_crec(const DevIndex &ix, uint32_t r, uint4 &r0, uint4 &r1) {
+    const uint4 *p = ix.crec + 2 * uint64_t(r);
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r0.x), "=r"(r0.y), "=r"(r0.z), "=r"(r0.w) : "l"(p));
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r1.x), "=r"(r1.y), "=r"(r1.z), "=r"(r1.w)
+                 : "l"(p + 1));
+}
+
 __device__ __forceinline__ uint32_t lds_volatile(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
 
 // STAGE: what of the index the CTAs keep in shared memory for their own
@@ -289,6 +299,9 @@ __global__ void __launch_bounds__(kClThreads, 1)
         if (ASYNC) {
             for (;;) {
                 const uint32_t p = sweeps & 1u;
+#ifdef EAT_CL_TRACE
+                const unsigned long long tr0 = gtimer();
+#endif
                 // ---- take every marked vertex this CTA owns
                 for (uint32_t lw = tid; lw < Wl; lw += kClThreads) {
                     if (!lds_volatile(bmN + lw)) continue;
@@ -306,6 +319,13 @@ __global__ void __launch_bounds__(kClThreads, 1)
                 __syncthreads();
                 const uint32_t F = s_cnt[p];
                 if (tid == 0) s_cnt[p ^ 1u] = 0;
+#ifdef EAT_CL_TRACE
+                if (tid == 0 && rank == 0 && sweeps < 1024) {
+                    g_cltrace[sweeps * 6 + 0] = tr0;
+                    g_cltrace[sweeps * 6 + 1] = gtimer();
+                    g_cltrace[sweeps * 6 + 5] = F;
+                }
+#endif
                 ++sweeps;
                 if (F == 0) {  // idle: is any vertex pending anywhere?
                     if (tid == 0) {
@@ -367,10 +387,15 @@ __global__ void __launch_bounds__(kClThreads, 1)
                                 tr.last |= cb & ix.zero;
                             }
                             if (eu <= tr.last) {
+                                // the hour-cluster record (one global access) is requested
+                                // before the DSMEM read of e[v]: the two latencies overlap
+                                uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = r0;
+                                const uint32_t kc = cluster_of(ix, eu);
+                                if (eu > tr.first) ldg_crec(ix, cb + kc, r0, r1);
                                 const uint32_t ea = e_addr(tr.v);
                                 const uint32_t av = cl_ld(ea);
                                 if (max(eu, tr.first) + tr.lam < av) {
-                                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_lookup(ix, cb, eu);
+                                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan(ix, r0, r1, kc, eu);
                                     const uint32_t cand = tc + tr.lam;
                                     if (cand < av && cand < cl_min(ea, cand)) mv = tr.v;
                                 }
@@ -382,6 +407,8 @@ __global__ void __launch_bounds__(kClThreads, 1)
                             if (lane == uint32_t(__ffs(wm) - 1)) {
                                 // returns once performed in CTA 0: every mark below is
                                 // counted before it can be seen (and un-counted) by its owner
+                                // (per-CTA counters read by a two-wave detector in CTA 0
+                                // instead: same speed, profiles/r02_ab_cluster_termination.jsonl)
                                 cl_add(pend0, uint32_t(__popc(wm)));
                             }
                             __syncwarp();
@@ -394,6 +421,9 @@ __global__ void __launch_bounds__(kClThreads, 1)
                 }
                 __syncthreads();  // every relaxation (and mark count) of the F taken vertices is done
                 if (tid == 0) cl_redadd(pend0, 0u - F);
+#ifdef EAT_CL_TRACE
+                if (tid == 0 && rank == 0 && sweeps - 1 < 1024) g_cltrace[(sweeps - 1) * 6 + 3] = gtimer();
+#endif
             }
         }
         for (; !ASYNC;) {
