@@ -85,9 +85,9 @@ enum {
 
 /* eat_build_opts.kernel: relaxation schedule for single queries. */
 enum {
-    EAT_KERNEL_AUTO = 0,          /* single queries: CTA kernel for graphs of <= 2048 stops, CLUSTER when the
-                                     whole index fits the shared memory of a 16-CTA cluster beside e[] (city
-                                     scale), else FRONTIER; batches: CTA when e[] fits shared memory */
+    EAT_KERNEL_AUTO = 0,          /* single queries: CTA kernel for graphs of <= 2048 stops, CLUSTER when e[]
+                                     and the type ranges fit the shared memory of a 16-CTA cluster (city,
+                                     metro), else FRONTIER; batches: CTA when e[] fits shared memory */
     EAT_KERNEL_FRONTIER = 1,      /* grid-wide persistent kernel, worklist frontier, global arr; requested
                                      explicitly, batches also run this schedule (CTA groups, e[] in global) */
     EAT_KERNEL_FULL_SWEEP = 2,    /* grid-wide persistent kernel, every type every sweep, active bitmap */
@@ -101,8 +101,10 @@ enum {
                                      by warps (warp per 32-vertex word, lanes over types); no worklist */
     EAT_KERNEL_CLUSTER = 7        /* one thread-block cluster of cluster_ctas CTAs (one per SM) per query,
                                      e[] and the frontier bitmaps distributed over the CTAs' shared memory
-                                     (DSMEM: ld / atom.min / red.or on the owner CTA), cluster barriers per
-                                     sweep; the CTA kernel's windowed schedule.  Needs |V| <= ~56k x CTAs */
+                                     (DSMEM: ld / atom.min / atom.or on the owner CTA), the owned sources'
+                                     index staged in shared memory; asynchronous: every CTA relaxes its
+                                     marked vertices on its own, termination by a pending-vertex counter
+                                     (no per-sweep barrier).  Needs e[] + ranges of |V| to fit 16 CTAs */
 };
 
 /* eat_build_opts.mode */
