@@ -608,15 +608,12 @@ def run_gpu(args):
     csa.close()
     del dev_rows
 
-    # ---- single-query latency (configs[1], [3], [4])
-    latency = _latency_legs(args, rank, world, dev, stream, flush, tt) if city else {}
-
     # ---- roofline of the batched kernel (rank 0)
     roof = _batch_roofline(tt, src, ts, dev, stream, args, step_ms, st0) if rank == 0 else None
 
+    line = None
     if rank == 0:
         resolved = _resolved(tt, all_ts) * args.steps
-        single = {k: v["s0_0600_ms"] for k, v in latency.items() if isinstance(v, dict) and "s0_0600_ms" in v}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
@@ -636,8 +633,8 @@ def run_gpu(args):
             "connections_resolved_per_s": resolved / (tot_ms / 1e3),
             "weak_scaling": weak,
             "variants": variants,
-            "single_query_ms": single,
-            "latency": latency,
+            "single_query_ms": None,
+            "latency": None,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(NQ * 8),
                     "d2h_bytes_per_step": int(NQ * tt.num_vertices * 4), "host_buffers": "pinned",
                     "rows_match_device_run": e2e_ok},
@@ -646,7 +643,36 @@ def run_gpu(args):
             "roofline": roof,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+
+    # ---- single-query latency (configs[1], [3], [4]) under a watchdog: the
+    # headline line above is complete, so a leg that fails or hangs (e.g. a
+    # collective of the N > 1 edge partition) costs only its own keys
+    emitted = threading.Lock()
+
+    def emit(lat):
+        if not emitted.acquire(blocking=False):
+            return False
+        if rank == 0:
+            line["latency"] = lat
+            line["single_query_ms"] = {k: v["s0_0600_ms"] for k, v in lat.items()
+                                       if isinstance(v, dict) and "s0_0600_ms" in v}
+            print(json.dumps(line), flush=True)
+        return True
+
+    def on_timeout():
+        if emit({"error": f"latency legs did not finish within {args.leg_timeout} s"}):
+            os._exit(0)
+
+    wd = threading.Timer(args.leg_timeout, on_timeout)
+    wd.daemon = True
+    wd.start()
+    try:
+        latency = _latency_legs(args, rank, world, dev, stream, flush, tt) if city else {}
+    except Exception as exc:  # noqa: BLE001 -- reported in the line
+        latency = {"error": repr(exc)[:300]}
+    wd.cancel()
+    if not emit(latency):
+        return
     if world > 1:
         import torch.distributed as dist
 
@@ -777,6 +803,8 @@ def main():
                     help="time budget of the all-cores oracle leg (its rows are the batch parity reference)")
     ap.add_argument("--ref-queries", type=int, default=0, help="--impl reference: queries per step (0: 128 x cores)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--leg-timeout", type=float, default=900.0,
+                    help="seconds the single-query latency legs may take before the line is printed without them")
     ap.add_argument("--fast", action="store_true", help="skip the sub-trip variants")
     ap.add_argument("--latency", default="city,metro,country",
                     help="single-query latency legs of the batch line (configs[1], [3], [4]); '' = none")
