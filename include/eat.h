@@ -116,6 +116,8 @@ enum {
 /* eat_build_opts.flags */
 #define EAT_BUILD_HOST_ONLY 0x1u   /* compress only, no device upload: introspection (eat_index_*) */
 #define EAT_BUILD_COUNTERS 0x2u    /* batched kernel runs its instrumented variant (work counters in eat_stats) */
+#define EAT_BUILD_CLUSTER_SYNC 0x8u /* EAT_KERNEL_CLUSTER: synchronous sweeps (one cluster barrier per sweep, the
+                                      time window) instead of the asynchronous default (results identical) */
 #define EAT_BUILD_MULTIPROCESS 0x4u /* EDGE_PARTITIONED + EAT_EXCHANGE_PEER: this process is rank part_rank of
                                        part_count processes (blocks joined with eat_peer_export/connect);
                                        without it all part_count partitions run in this process (loopback) */

@@ -27,6 +27,7 @@ EAT_MODE = {"replicated": 0, "edge_partitioned": 1}
 EAT_BUILD_HOST_ONLY = 0x1
 EAT_BUILD_COUNTERS = 0x2
 EAT_BUILD_MULTIPROCESS = 0x4
+EAT_BUILD_CLUSTER_SYNC = 0x8
 EAT_EXCHANGE = {"allreduce": 0, "peer": 1}
 EAT_PEER_HANDLE_BYTES = 64
 

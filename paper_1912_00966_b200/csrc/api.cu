@@ -133,7 +133,7 @@ struct eat_handle {
     uint32_t single_cta_threads = 1024;  // CTA variant of a lone query: 1024 when it fits, else cta_threads
     uint32_t cluster_ctas = 0;           // EAT_KERNEL_CLUSTER: CTAs per cluster (resolved at build)
     int cluster_stage = 0;               // ... index staged in shared memory (cluster.cu STAGE)
-    bool cluster_async = !getenv("EAT_CLUSTER_ASYNC") || atoi(getenv("EAT_CLUSTER_ASYNC")) != 0;  // A/B knob (default on)
+    bool cluster_async = true;           // EAT_KERNEL_CLUSTER: asynchronous (EAT_BUILD_CLUSTER_SYNC: sweeps)
     uint32_t cluster_window = EAT_INF;   // ... schedule window (all active vertices unless set: fastest, r02_cluster_*)
     uint32_t cluster_tl = 0;             // ... most types owned by one CTA
     bool batch_groups = false;  // batches on k_query_groups even when e[] fits shared memory (kernel FRONTIER)
@@ -668,6 +668,7 @@ eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
     h->loopback = o.mode == EAT_MODE_EDGE_PARTITIONED && pc > 1 &&
                   (o.exchange == EAT_EXCHANGE_PEER ? !(o.flags & EAT_BUILD_MULTIPROCESS) : !o.nccl_unique_id);
     h->host_only = (o.flags & EAT_BUILD_HOST_ONLY) != 0;
+    h->cluster_async = !(o.flags & EAT_BUILD_CLUSTER_SYNC) && !(getenv("EAT_CLUSTER_ASYNC") && atoi(getenv("EAT_CLUSTER_ASYNC")) == 0);
     h->lookup_mode = o.lookup;
     return EAT_OK;
 }

@@ -68,7 +68,7 @@ class Engine:
                  cta_threads: int = 0, subtrips: int = 0, trip=None, arr_bits: int = 0,
                  cluster_dir: str = "auto", lookup: str = "cluster_ap", continuation: Optional[int] = None,
                  exchange: str = "allreduce", multiprocess: bool = False, local_sweeps: int = 0,
-                 devices=None, cluster_ctas: int = 0):
+                 devices=None, cluster_ctas: int = 0, cluster_sync: bool = False):
         self._h = None
         arrs = [_u32(u), _u32(v), _u32(dep), _u32(dur)]
         m = arrs[0].shape[0]
@@ -92,7 +92,8 @@ class Engine:
                                    device=int(device), kernel=_lib.EAT_KERNEL[kernel],
                                    flags=(_lib.EAT_BUILD_HOST_ONLY if host_only else 0)
                                    | (_lib.EAT_BUILD_COUNTERS if counters else 0)
-                                   | (_lib.EAT_BUILD_MULTIPROCESS if multiprocess else 0), subwarp=int(subwarp),
+                                   | (_lib.EAT_BUILD_MULTIPROCESS if multiprocess else 0)
+                                   | (_lib.EAT_BUILD_CLUSTER_SYNC if cluster_sync else 0), subwarp=int(subwarp),
                                    mode=_lib.EAT_MODE[mode], part_rank=int(part_rank), part_count=int(part_count),
                                    nccl_unique_id=ctypes.cast(self._nccl_buf, ctypes.c_void_p) if self._nccl_buf else None,
                                    window_seconds=int(window), cta_threads=int(cta_threads),

@@ -248,7 +248,8 @@ def test_cluster_kernel_sizes(ctas):
     for name in ("tiny", "city"):
         tt = synth.generate(name)
         csa = oracle.CSA(tt.num_vertices, *tt.arrays())
-        eng = Engine.from_timetable(tt, kernel="cluster", cluster_ctas=ctas, subtrips=3)
+        eng = Engine.from_timetable(tt, kernel="cluster", cluster_ctas=ctas, subtrips=3,
+                                    cluster_sync=(ctas == 4))  # the synchronous variant too
         st = eng.stats()
         assert st["kernel_name"] == "cluster" and st["cluster_ctas"] == ctas
         rng = np.random.default_rng(ctas)

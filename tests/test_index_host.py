@@ -182,6 +182,13 @@ def test_build_errors():
     with pytest.raises(EatError) as e:
         Engine(3, [0], [1], [5], [10], host_only=True, subwarp=3)
     assert e.value.status == _lib.EAT_EINVAL
+    for bad in (1, 3, 32):  # EAT_KERNEL_CLUSTER sizes: 2, 4, 8 or 16 CTAs
+        with pytest.raises(EatError) as e:
+            Engine(3, [0], [1], [5], [10], host_only=True, cluster_ctas=bad)
+        assert e.value.status == _lib.EAT_EINVAL
+    with pytest.raises(EatError) as e:
+        Engine(3, [0], [1], [5], [10], host_only=True, cta_threads=300)
+    assert e.value.status == _lib.EAT_EINVAL
     eng = Engine(3, [0], [1], [5], [10], host_only=True)
     with pytest.raises(EatError) as e:
         eng.query(0, 0)
