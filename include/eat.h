@@ -99,12 +99,16 @@ enum {
                                      connection every sweep (Algorithm 4) */
     EAT_KERNEL_BITMAP = 6,        /* grid-wide persistent kernel, global arr, active-vertex bitmap scanned
                                      by warps (warp per 32-vertex word, lanes over types); no worklist */
-    EAT_KERNEL_CLUSTER = 7        /* one thread-block cluster of cluster_ctas CTAs (one per SM) per query,
+    EAT_KERNEL_CLUSTER = 7,       /* one thread-block cluster of cluster_ctas CTAs (one per SM) per query,
                                      e[] and the frontier bitmaps distributed over the CTAs' shared memory
                                      (DSMEM: ld / atom.min / atom.or on the owner CTA), the owned sources'
                                      index staged in shared memory; asynchronous: every CTA relaxes its
                                      marked vertices on its own, termination by a pending-vertex counter
                                      (no per-sweep barrier).  Needs e[] + ranges of |V| to fit 16 CTAs */
+    EAT_KERNEL_GRID_ASYNC = 8     /* the asynchronous schedule on the whole GPU: persistent cooperative grid,
+                                     global e[] and marked bitmap (word w owned by CTA w mod grid), every CTA
+                                     relaxes its marked vertices on its own; termination by per-CTA mark /
+                                     done counters and a two-wave detector; no barrier between relaxations */
 };
 
 /* eat_build_opts.mode */

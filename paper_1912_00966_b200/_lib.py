@@ -21,7 +21,7 @@ STATUS_NAMES = ["EAT_OK", "EAT_EINVAL", "EAT_ERANGE", "EAT_ENOMEM", "EAT_ECUDA",
 
 EAT_RENUMBER = {"auto": 0, "none": 1, "bfs": 2, "morton": 3}
 EAT_KERNEL = {"auto": 0, "frontier": 1, "full_sweep": 2, "cta": 3, "async": 4, "connection": 5, "bitmap": 6,
-              "cluster": 7}
+              "cluster": 7, "grid_async": 8}
 EAT_KERNEL_NAMES = {v: k for k, v in EAT_KERNEL.items()}
 EAT_MODE = {"replicated": 0, "edge_partitioned": 1}
 EAT_BUILD_HOST_ONLY = 0x1

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "eat")
 LIB = os.path.join(PKG, "libeat.so")
-SOURCES = ["build.cpp", "kernels.cu", "partition.cu", "async.cu", "peer.cu", "cluster.cu", "api.cu"]
+SOURCES = ["build.cpp", "kernels.cu", "partition.cu", "async.cu", "peer.cu", "cluster.cu", "gasync.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -96,6 +96,9 @@ struct eat_handle {
     bool loopback = false;
     // single-query scratch
     eat::GridWork gw{};
+    uint32_t *d_gacnt = nullptr;         // EAT_KERNEL_GRID_ASYNC: per-CTA counters
+    int gasync_stage = 1;                // ... index staged in shared memory (gasync.cu STAGE)
+    uint32_t gasync_tl = 0;              // ... most types owned by one CTA (stage 2)
     std::vector<eat::GridWork> bgw;   // batched queries without shared-memory e[]: one scratch per CTA group
     eat::GridWork *d_bgw = nullptr;
     eat::AsyncWork aw{};
@@ -190,6 +193,8 @@ void release_device(eat_handle *h) {
     if (h->host_only) return;
     cudaSetDevice(h->device);
     gridwork_free(h->gw);
+    if (h->d_gacnt) cudaFree(h->d_gacnt);
+    h->d_gacnt = nullptr;
     for (eat::GridWork &w : h->bgw) gridwork_free(w);
     if (h->d_bgw) cudaFree(h->d_bgw);
     if (h->d_srows) cudaFree(h->d_srows);
@@ -495,6 +500,30 @@ bool pick_cluster(eat_handle *h, uint32_t want, int min_stage) {
     return false;
 }
 
+// EAT_KERNEL_GRID_ASYNC configuration: the deepest staging that fits (2 =
+// headers on chip, 1 = type ranges only) and the per-CTA counters.
+bool pick_gasync(eat_handle *h) {
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) return false;
+    const char *env = getenv("EAT_GASYNC_STAGE");  // A/B knob: highest staging level tried
+    const int max_stage = env ? std::max(1, std::min(2, atoi(env))) : 2;
+    const uint32_t tl = cluster_tl_cap(h->hx, uint32_t(sms));  // same word-interleaved ownership
+    int G = 0;
+    if (max_stage == 2 && (G = eat::gasync_grid(h->hx.n, 2, tl)) > 0) {
+        h->gasync_stage = 2;
+        h->gasync_tl = tl;
+    } else if ((G = eat::gasync_grid(h->hx.n, 1, 0)) > 0) {
+        h->gasync_stage = 1;
+        h->gasync_tl = 0;
+    } else {
+        return false;
+    }
+    if (!h->d_gacnt && cudaMalloc(&h->d_gacnt, size_t(G) * 32u * sizeof(uint32_t)) != cudaSuccess) return false;
+    return true;
+}
+
 eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     h->cta_grid = eat::cta_grid_size(h->hx.n, int(h->cta_threads), h->arr16);
     // a lone query takes the widest CTA (1024 threads, uint32 e[]) when its
@@ -528,7 +557,9 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CTA: arrival array does not fit shared memory");
     if (k == EAT_KERNEL_ASYNC && !async_ok)
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_ASYNC: a 1/SM-count slice of the arrival array does not fit shared memory");
-    if (k > EAT_KERNEL_CLUSTER) return fail(EAT_EINVAL, "unknown kernel");
+    if (k > EAT_KERNEL_GRID_ASYNC) return fail(EAT_EINVAL, "unknown kernel");
+    if (k == EAT_KERNEL_GRID_ASYNC && !pick_gasync(h))
+        return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_GRID_ASYNC: the per-CTA vertex slices do not fit shared memory");
     if (k == EAT_KERNEL_CLUSTER && !pick_cluster(h, h->cluster_ctas, 0))
         return fail(EAT_EUNSUPPORTED, "EAT_KERNEL_CLUSTER: e[] does not fit the shared memory of a schedulable cluster");
     if (k == EAT_KERNEL_CONNECTION) {  // raw connections on the device (ablation schedule)
@@ -596,6 +627,10 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
         eat::DevIndex cix = h->ix;
         cix.window = h->cluster_window;
         CUDA_TRY(eat::launch_query_cluster(cix, a, st));
+    } else if (h->kernel == EAT_KERNEL_GRID_ASYNC) {
+        eat::GAsyncWork w{h->gw.arr, h->gw.bm, h->d_gacnt, h->gw.ctl, h->gasync_stage, h->gasync_tl};
+        CUDA_TRY(eat::launch_query_gasync(h->ix, w, s, t_s, d_out, st));
+        CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->gw.ctl + 8, 4, cudaMemcpyDeviceToDevice, st));
     } else if (h->kernel == EAT_KERNEL_ASYNC) {
         CUDA_TRY(eat::launch_query_async(h->ix, h->aw, s, t_s, d_out, st));
         CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->aw.ctl + 9, 4, cudaMemcpyDeviceToDevice, st));
@@ -631,7 +666,7 @@ eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
     if (sw != 0 && sw != 1 && sw != 2 && sw != 4 && sw != 8 && sw != 16 && sw != 32)
         return fail(EAT_EINVAL, "subwarp must be 0 (default 32), 1, 2, 4, 8, 16, 32 or 64 (flattened pairs)");
     if (o.mode > EAT_MODE_EDGE_PARTITIONED) return fail(EAT_EINVAL, "unknown mode");
-    if (o.kernel > EAT_KERNEL_CLUSTER) return fail(EAT_EINVAL, "unknown kernel");
+    if (o.kernel > EAT_KERNEL_GRID_ASYNC) return fail(EAT_EINVAL, "unknown kernel");
     if (o.lookup > 2) return fail(EAT_EINVAL, "lookup must be 0 (Cluster-AP), 1 (Connection-type-AP) or 2 (linear)");
     const uint32_t pc = o.part_count ? o.part_count : 1;
     if (o.mode == EAT_MODE_EDGE_PARTITIONED && o.part_rank >= pc)

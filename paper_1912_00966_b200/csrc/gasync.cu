@@ -1,0 +1,313 @@
+// gasync.cu -- EAT_KERNEL_GRID_ASYNC: one query on the whole GPU without any
+// barrier between relaxations.
+//
+// The asynchronous schedule of the cluster kernel (cluster.cu ASYNC) over
+// global memory, so that graphs whose e[] does not fit a cluster (country)
+// and the whole GPU's SMs can use it: a persistent cooperative grid of
+// 1024-thread CTAs, one per SM.  e[] and the "marked" bitmap live in global
+// memory; bitmap word w (vertices 32w .. 32w+31) is owned by CTA w mod G.
+// Every CTA loops on its own:
+//   take every marked vertex it owns (atomicExch on its bitmap words, so a
+//   mark may land at any time) -> relax their connection types (Alg. 3,
+//   PAPER.md:175-190; Cluster-AP lookup, Alg. 6 + PAPER.md:300-306;
+//   atomicMin on e[v]) -> mark every v it lowered;
+// all active vertices are taken (the paper's topology-driven schedule, any
+// order reaches the same fixpoint).
+// Termination (no barrier to count "nothing changed" at): per CTA, S counts
+// the marks it set (incremented with a returning atomic BEFORE the bits are
+// set, decremented for marks that hit an already-set bit) and R the vertices
+// whose relaxations it finished.  When CTA 0 is idle it sums every R, then
+// every S; both are monotone in the true counts and a mark is counted in S
+// before its bit is visible, so sum(R) read first == sum(S) read second means
+// nothing was marked or in processing at any instant between the two reads
+// -- and a fixpoint is stable: it raises the done flag every idle CTA polls.
+// Grid barriers only around a query (initialization, output).
+#include <algorithm>
+
+#include "device_common.cuh"
+#include "kernels.cuh"
+
+namespace eat {
+namespace {
+
+using namespace dev;
+
+constexpr uint32_t kGaCntStride = 32;  // S, R of CTA c at cnt[c * 32 + 0 / 1] (own 128-byte line)
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) { return __ldcv(p); }  // fetched again (L2)
+
+// 32-byte cluster record r as volatile loads (issued where written)
+__device__ __forceinline__ void ldg_crec_ga(const DevIndex &ix, uint32_t r, uint4 &r0, uint4 &r1) {
+    const uint4 *p = ix.crec + 2 * uint64_t(r);
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r0.x), "=r"(r0.y), "=r"(r0.z), "=r"(r0.w) : "l"(p));
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r1.x), "=r"(r1.y), "=r"(r1.z), "=r"(r1.w)
+                 : "l"(p + 1));
+}
+
+// STAGE 2: the 16-byte headers and cluster bases of the owned vertices'
+// types are also staged in shared memory (when they fit: metro), so a
+// relaxation's only index access off chip is its hour-cluster record.
+constexpr int kGaThreads = 1024;  // one CTA per SM (512 x 2 ... 256 x 8 within +-3 %: r02_gasync_shape.jsonl)
+constexpr uint32_t kGaWarps = kGaThreads / 32;
+
+template <int STAGE>
+__global__ void __launch_bounds__(kGaThreads, 1)
+    k_query_gasync(DevIndex ix, GAsyncWork w, uint32_t s, uint32_t ts, uint32_t *__restrict__ out, uint32_t tl_cap) {
+    extern __shared__ uint4 sm4[];
+    const uint32_t n = ix.n, G = gridDim.x, c = blockIdx.x;
+    const uint32_t W = (n + 31u) / 32u;
+    const uint32_t Wl = (W + G - 1u) / G;                      // words owned by this CTA (some may be >= W)
+    // layout: hdr_s[tl_cap] | rng[32 Wl] | list[32 Wl] | cb_s[tl_cap] | wst[Wl]
+    uint4 *hdr_s = sm4;                                                          // STAGE 2
+    uint2 *rng = reinterpret_cast<uint2 *>(sm4 + (STAGE == 2 ? tl_cap : 0u));   // type range of every owned vertex
+    uint32_t *list = reinterpret_cast<uint32_t *>(rng + Wl * 32u);               // taken vertices
+    uint32_t *cb_s = list + Wl * 32u;                                            // STAGE 2
+    uint32_t *wst = cb_s + (STAGE == 2 ? tl_cap : 0u);                           // STAGE 2: local start per word
+    __shared__ uint32_t s_cnt[2];
+    __shared__ uint32_t s_done;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+    const uint64_t gtid = uint64_t(c) * kGaThreads + tid, gsz = uint64_t(G) * kGaThreads;
+    uint32_t *bar = w.ctl + kBarWord;  // monotonic grid-barrier counter (zeroed per launch)
+    uint32_t bar_epoch = 0;
+    uint32_t *myS = w.cnt + c * kGaCntStride, *myR = myS + 1;
+
+    // ---- stage the owned vertices' index; initialize (Alg. 2)
+    auto wrange = [&](uint32_t lw, uint32_t &g0, uint32_t &g1) {  // global type range of owned word lw
+        const uint32_t gw = lw * G + c;
+        g0 = __ldg(ix.type_ptr + min(32u * gw, n));
+        g1 = __ldg(ix.type_ptr + min(32u * gw + 32u, n));
+    };
+    if (STAGE == 2) {
+        if (wid == 0) {  // local start of each owned word's types
+            const uint32_t per = (Wl + 31u) / 32u, lo = min(Wl, lane * per), hi = min(Wl, lo + per);
+            uint32_t sum = 0, g0, g1;
+            for (uint32_t lw = lo; lw < hi; ++lw) {
+                wrange(lw, g0, g1);
+                sum += g1 - g0;
+            }
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= uint32_t(o)) incl += y;
+            }
+            uint32_t run = incl - sum;
+            for (uint32_t lw = lo; lw < hi; ++lw) {
+                wrange(lw, g0, g1);
+                wst[lw] = run;
+                run += g1 - g0;
+            }
+        }
+        __syncthreads();
+        for (uint32_t lw = wid; lw < Wl; lw += kGaWarps) {  // a warp per owned word
+            uint32_t g0, g1;
+            wrange(lw, g0, g1);
+            for (uint32_t t = g0 + lane; t < g1; t += 32u) {
+                hdr_s[wst[lw] + t - g0] = __ldg(ix.type_hdr + t);
+                cb_s[wst[lw] + t - g0] = __ldg(ix.type_cb + t);
+            }
+        }
+    }
+    for (uint32_t li = tid; li < Wl * 32u; li += kGaThreads) {
+        const uint32_t gw = (li >> 5) * G + c, v = gw * 32u + (li & 31u);
+        uint2 r = make_uint2(0u, 0u);
+        if (v < n) {
+            const uint32_t a = __ldg(ix.type_ptr + v);
+            r = make_uint2(a, __ldg(ix.type_ptr + v + 1) - a);
+            if (STAGE == 2) r.x = wst[li >> 5] + (a - __ldg(ix.type_ptr + 32u * gw));  // local type index
+        }
+        rng[li] = r;
+    }
+    for (uint64_t i = gtid; i < n; i += gsz) w.arr[i] = kInf;
+    for (uint64_t i = gtid; i < W; i += gsz) w.bm[i] = 0;
+    if (tid == 0) {
+        myS[0] = 0;
+        myR[0] = 0;
+        s_cnt[0] = s_cnt[1] = 0;
+        s_done = 0;
+    }
+    if (gtid == 0) w.ctl[0] = 0;  // done flag
+    grid_sync(bar, bar_epoch, G);
+    if (gtid == 0) {
+        const uint32_t si = __ldg(ix.perm + s);
+        w.arr[si] = ts;
+        w.bm[si >> 5] = 1u << (si & 31u);
+        atomicAdd(w.cnt + ((si >> 5) % G) * kGaCntStride, 1u);  // the source's mark, counted by its owner
+    }
+    grid_sync(bar, bar_epoch, G);
+
+    uint32_t iters = 0;
+    for (;;) {
+        const uint32_t p = iters & 1u;
+        ++iters;
+        // ---- take every marked vertex this CTA owns
+        for (uint32_t lw = tid; lw < Wl; lw += kGaThreads) {
+            const uint32_t gw = lw * G + c;
+            if (gw >= W || !ld_volatile(w.bm + gw)) continue;
+            uint32_t word = atomicExch(w.bm + gw, 0u);
+            const uint32_t k = __popc(word);
+            if (!k) continue;
+            const uint32_t pos = atomicAdd(&s_cnt[p], k);  // the list holds every owned vertex
+            for (uint32_t i = 0; i < k; ++i) {
+                const uint32_t b = __ffs(word) - 1u;
+                word &= word - 1u;
+                list[pos + i] = (lw << 5) | b;  // local index
+            }
+        }
+        __syncthreads();
+        const uint32_t F = s_cnt[p];
+        if (tid == 0) s_cnt[p ^ 1u] = 0;
+        if (F == 0) {  // idle: termination detection (CTA 0) / poll
+            if (wid == 0) {
+                if (c == 0) {
+                    uint32_t ra = 0, sb = 0;
+                    for (uint32_t x = lane; x < G; x += 32u) ra += ld_volatile(w.cnt + x * kGaCntStride + 1);
+                    ra = __reduce_add_sync(0xFFFFFFFFu, ra);
+                    for (uint32_t x = lane; x < G; x += 32u) sb += ld_volatile(w.cnt + x * kGaCntStride);
+                    sb = __reduce_add_sync(0xFFFFFFFFu, sb);
+                    if (lane == 0 && ra == sb) __stcg(w.ctl, 1u);
+                }
+                if (lane == 0) {
+                    s_done = ld_volatile(w.ctl);
+                    if (!s_done) __nanosleep(100);
+                }
+            }
+            __syncthreads();
+            if (s_done || iters > (1u << 22)) break;  // (watchdog: never reached by a correct run)
+            continue;
+        }
+        const uint32_t g = min(32u, max(1u, (F + kGaWarps - 1u) / kGaWarps));
+        for (uint32_t k0 = wid * g; k0 < F; k0 += kGaWarps * g) {
+            const uint32_t j = k0 + lane;
+            uint32_t x = 0, p0 = 0, nt = 0;  // x: global vertex id
+            if (lane < g && j < F) {
+                const uint32_t li = list[j];
+                x = ((li >> 5) * G + c) * 32u + (li & 31u);
+                const uint2 r = rng[li];
+                p0 = r.x;
+                nt = r.y;
+            }
+            uint32_t incl = nt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= uint32_t(o)) incl += y;
+            }
+            const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            for (uint32_t base = 0; base < tot; base += 32u) {
+                const uint32_t qp = base + lane;
+                uint32_t L = 0;
+#pragma unroll
+                for (uint32_t step = 16; step > 0; step >>= 1) {
+                    const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, L + step - 1u);
+                    if (v <= qp) L += step;
+                }
+                const uint32_t o_incl = __shfl_sync(0xFFFFFFFFu, incl, L);
+                const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
+                const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
+                const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
+                uint32_t mv = kNone;  // vertex this lane lowered (to be marked)
+                if (qp < tot) {
+                    const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
+                    const uint32_t eu = __ldcg(w.arr + u);
+                    uint32_t cb;
+                    TypeRec tr;
+                    if (STAGE == 2) {  // t is a local type index
+                        cb = cb_s[t];
+                        const uint4 h = hdr_s[t];
+                        tr = TypeRec{h.x, h.y, h.z, h.w};
+                    } else {
+                        cb = __ldg(ix.type_cb + t);
+                        tr = load_type(ix, t);
+                        tr.last |= cb & ix.zero;
+                    }
+                    if (eu <= tr.last) {
+                        uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = r0;
+                        const uint32_t kc = cluster_of(ix, eu);
+                        if (eu > tr.first) ldg_crec_ga(ix, cb + kc, r0, r1);  // overlaps the e[v] read
+                        const uint32_t av = __ldcg(w.arr + tr.v);
+                        if (max(eu, tr.first) + tr.lam < av) {
+                            const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan(ix, r0, r1, kc, eu);
+                            const uint32_t cand = tc + tr.lam;
+                            if (cand < av && cand < atomicMin(w.arr + tr.v, cand)) mv = tr.v;
+                        }
+                    }
+                }
+                const uint32_t wm = __ballot_sync(0xFFFFFFFFu, mv != kNone);
+                if (wm) {
+                    // counted in S (returning atomic: performed) before any bit is set
+                    if (lane == uint32_t(__ffs(wm) - 1)) atomicAdd(myS, uint32_t(__popc(wm)));
+                    __syncwarp();
+                    uint32_t dup = 0;
+                    if (mv != kNone) dup = atomicOr(w.bm + (mv >> 5), 1u << (mv & 31u)) & (1u << (mv & 31u));
+                    const uint32_t dm = __ballot_sync(0xFFFFFFFFu, dup != 0u);
+                    if (dm && lane == uint32_t(__ffs(dm) - 1)) atomicSub(myS, uint32_t(__popc(dm)));
+                }
+            }
+        }
+        __syncthreads();  // every relaxation (and its mark count) of the F taken vertices is done
+        if (tid == 0) atomicAdd(myR, F);
+    }
+    if (gtid == 0) w.ctl[8] = iters;  // rank 0's iterations (eat_stats.last_sweeps)
+    grid_sync(bar, bar_epoch, G);
+    // ---- output in caller ids (16-byte stores when aligned)
+    if ((n & 3u) == 0u && (reinterpret_cast<uintptr_t>(out) & 15u) == 0u) {
+        const uint4 *pv = reinterpret_cast<const uint4 *>(ix.perm);
+        uint4 *ov = reinterpret_cast<uint4 *>(out);
+        for (uint64_t i = gtid; i < n / 4u; i += gsz) {
+            const uint4 pi = __ldg(pv + i);
+            ov[i] = make_uint4(__ldcg(w.arr + pi.x), __ldcg(w.arr + pi.y), __ldcg(w.arr + pi.z), __ldcg(w.arr + pi.w));
+        }
+    } else {
+        for (uint64_t i = gtid; i < n; i += gsz) out[i] = __ldcg(w.arr + __ldg(ix.perm + i));
+    }
+}
+
+size_t gasync_smem(uint32_t n, int G, int stage, uint32_t tl_cap) {
+    const size_t W = (n + 31u) / 32u, Wl = (W + size_t(G) - 1u) / size_t(G);
+    size_t b = Wl * 32u * (8u + 4u);
+    if (stage == 2) b += size_t(tl_cap) * 20u + Wl * 4u;
+    return b;
+}
+
+template <int STAGE>
+int gasync_grid_t(uint32_t n, uint32_t tl_cap) {
+    auto kern = k_query_gasync<STAGE>;
+    int dev = 0, sms = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 0;
+    const size_t smem = gasync_smem(n, sms, STAGE, tl_cap);
+    if (smem + fa.sharedSizeBytes > size_t(optin)) return 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 0;
+    int per_sm = 0;  // every CTA must be resident (they wait on each other): one per SM
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGaThreads, smem) != cudaSuccess || per_sm < 1)
+        return 0;
+    return sms;
+}
+
+}  // namespace
+
+int gasync_grid(uint32_t n, int stage, uint32_t tl_cap) {
+    return stage == 2 ? gasync_grid_t<2>(n, tl_cap) : gasync_grid_t<1>(n, 0);
+}
+
+cudaError_t launch_query_gasync(const DevIndex &ix, const GAsyncWork &w, uint32_t s, uint32_t t_s, uint32_t *d_out,
+                                cudaStream_t st) {
+    const int G = gasync_grid(ix.n, w.stage, w.tl_cap);
+    if (G < 1) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaMemsetAsync(w.ctl + kBarWord, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    DevIndex ixc = ix;
+    GAsyncWork wc = w;
+    uint32_t tl = w.tl_cap;
+    void *args[] = {&ixc, &wc, &s, &t_s, &d_out, &tl};
+    const void *kern = w.stage == 2 ? (const void *)k_query_gasync<2> : (const void *)k_query_gasync<1>;
+    return cudaLaunchCooperativeKernel(kern, dim3(unsigned(G)), dim3(kGaThreads), args,
+                                       gasync_smem(ix.n, G, w.stage, w.tl_cap), st);
+}
+
+}  // namespace eat

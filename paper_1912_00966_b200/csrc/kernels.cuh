@@ -139,6 +139,20 @@ cudaError_t launch_query_cluster(const DevIndex &ix, const ClusterArgs &a, cudaS
 // Co-resident clusters of cs CTAs for n vertices at a staging level (0: does not fit / not schedulable).
 int cluster_max_active(uint32_t n, int cs, int stage, uint32_t tl_cap, bool async);
 
+// Scratch of the barrier-free grid kernel (gasync.cu, EAT_KERNEL_GRID_ASYNC).
+struct GAsyncWork {
+    uint32_t *arr;   // [n] arrival times, internal ids
+    uint32_t *bm;    // [W] marked-vertex bitmap
+    uint32_t *cnt;   // [32 * grid] per-CTA counters: S (marks set), R (vertices done)
+    uint32_t *ctl;   // [kCtlWords]: 0 done flag, 8 iterations of CTA 0, kBarWord grid barrier
+    int stage;       // 1: type ranges staged in shared memory; 2: + headers and cluster bases
+    uint32_t tl_cap; // stage 2: most types owned by one CTA
+};
+// CTAs of the launch for n vertices at a staging level (one per SM; 0 if it does not fit shared memory).
+int gasync_grid(uint32_t n, int stage, uint32_t tl_cap);
+cudaError_t launch_query_gasync(const DevIndex &ix, const GAsyncWork &w, uint32_t s, uint32_t t_s, uint32_t *d_out,
+                                cudaStream_t st);
+
 // CTAs per SM of the persistent grid kernels (env EAT_GRID_CTAS_PER_SM, default 1).
 int grid_ctas_per_sm();
 

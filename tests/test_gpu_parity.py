@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_1912_00966_b200 import Engine, EatError, _lib  # noqa: E402
 
-KERNELS = ["cta", "frontier", "full_sweep", "async", "bitmap", "cluster"]
+KERNELS = ["cta", "frontier", "full_sweep", "async", "bitmap", "cluster", "grid_async"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -234,7 +234,7 @@ def test_metro_single_query():
     csa = oracle.CSA(tt.num_vertices, *tt.arrays())
     for s, t_s in [synth.SINGLE_QUERY, (777, 30000)]:
         _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"metro ({s},{t_s})")
-    for kernel in ("frontier", "async", "cluster"):
+    for kernel in ("frontier", "async", "cluster", "grid_async"):
         e2 = Engine.from_timetable(tt, kernel=kernel)
         for s, t_s in [synth.SINGLE_QUERY, (91, 50000)]:
             _assert_rows(e2.query(s, t_s), csa.query(s, t_s), f"metro {kernel} ({s},{t_s})")
@@ -536,7 +536,7 @@ def test_country_single_query():
     qs = [synth.SINGLE_QUERY] + [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 86400))) for _ in range(3)]
     want = [csa.query(*q) for q in qs]
     csa.close()
-    for kw in ({"subtrips": 3}, {"mode": "edge_partitioned", "part_count": 1},
+    for kw in ({"subtrips": 3}, {"subtrips": 3, "kernel": "grid_async"}, {"mode": "edge_partitioned", "part_count": 1},
                {"mode": "edge_partitioned", "part_count": 2, "subtrips": 3},
                {"mode": "edge_partitioned", "part_count": 2, "exchange": "peer", "subtrips": 3}):
         eng = Engine.from_timetable(tt, **kw)

@@ -33,11 +33,16 @@ torch.cuda.synchronize()
 sw = eng.stats()["last_sweeps"]
 buf = (ctypes.c_ulonglong * (1024 * 6))()
 _lib.lib().eat_debug_cluster_trace(buf, 1024 * 6)
-t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 6)[:sw].astype(np.int64)
-d = {"select": np.diff(t[:, [0, 1]]).ravel(), "barrier1": np.diff(t[:, [1, 2]]).ravel(),
-     "pairs": np.diff(t[:, [2, 3]]).ravel(), "push_barrier2": np.diff(t[:, [3, 4]]).ravel()}
+t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 6)[:min(sw, 1024)].astype(np.int64)
+if os.environ.get("EAT_CLUSTER_ASYNC", "1") != "0":  # asynchronous loop: start, after select, after pairs, F
+    busy = t[:, 5] > 0
+    d = {"select": np.diff(t[:, [0, 1]]).ravel(), "pairs": np.diff(t[busy][:, [1, 3]]).ravel(),
+         "F": t[busy, 5].astype(np.float64), "idle_iterations": np.array([float((~busy).sum())])}
+else:
+    d = {"select": np.diff(t[:, [0, 1]]).ravel(), "barrier1": np.diff(t[:, [1, 2]]).ravel(),
+         "pairs": np.diff(t[:, [2, 3]]).ravel(), "push_barrier2": np.diff(t[:, [3, 4]]).ravel()}
 d["sweep"] = np.diff(t[:, 0]) if sw > 1 else np.array([0])
 print(json.dumps({"cfg": cfg, "cluster_ctas": eng.stats()["cluster_ctas"], "window": window, "sweeps": int(sw),
                   "ns_mean": {k: float(v.mean()) for k, v in d.items()},
                   "ns_p90": {k: float(np.percentile(v, 90)) for k, v in d.items()},
-                  "first_sweeps_ns": t[:8, :5].tolist()}))
+                  "first_sweeps_ns": t[:8, :6].tolist()}))
