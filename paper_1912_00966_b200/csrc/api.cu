@@ -97,8 +97,6 @@ struct eat_handle {
     // single-query scratch
     eat::GridWork gw{};
     uint32_t *d_gacnt = nullptr;         // EAT_KERNEL_GRID_ASYNC: per-CTA counters
-    int gasync_stage = 1;                // ... index staged in shared memory (gasync.cu STAGE)
-    uint32_t gasync_tl = 0;              // ... most types owned by one CTA (stage 2)
     std::vector<eat::GridWork> bgw;   // batched queries without shared-memory e[]: one scratch per CTA group
     eat::GridWork *d_bgw = nullptr;
     eat::AsyncWork aw{};
@@ -500,26 +498,10 @@ bool pick_cluster(eat_handle *h, uint32_t want, int min_stage) {
     return false;
 }
 
-// EAT_KERNEL_GRID_ASYNC configuration: the deepest staging that fits (2 =
-// headers on chip, 1 = type ranges only) and the per-CTA counters.
+// EAT_KERNEL_GRID_ASYNC: fits (per-CTA slices in shared memory) + per-CTA counters.
 bool pick_gasync(eat_handle *h) {
-    int sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms < 1) return false;
-    const char *env = getenv("EAT_GASYNC_STAGE");  // A/B knob: highest staging level tried
-    const int max_stage = env ? std::max(1, std::min(2, atoi(env))) : 2;
-    const uint32_t tl = cluster_tl_cap(h->hx, uint32_t(sms));  // same word-interleaved ownership
-    int G = 0;
-    if (max_stage == 2 && (G = eat::gasync_grid(h->hx.n, 2, tl)) > 0) {
-        h->gasync_stage = 2;
-        h->gasync_tl = tl;
-    } else if ((G = eat::gasync_grid(h->hx.n, 1, 0)) > 0) {
-        h->gasync_stage = 1;
-        h->gasync_tl = 0;
-    } else {
-        return false;
-    }
+    const int G = eat::gasync_grid(h->hx.n);
+    if (G < 1) return false;
     if (!h->d_gacnt && cudaMalloc(&h->d_gacnt, size_t(G) * 32u * sizeof(uint32_t)) != cudaSuccess) return false;
     return true;
 }
@@ -544,11 +526,14 @@ eat_status resolve_kernel(eat_handle *h, uint32_t requested) {
     // when e[] fits (throughput).
     if (k == EAT_KERNEL_AUTO) {
         if (h->cta_grid > 0 && h->hx.n <= kAutoCtaMaxVertices) k = EAT_KERNEL_CTA;
-        // graphs whose e[] and type ranges fit the shared memory of a 16-CTA
-        // cluster: the (asynchronous) cluster kernel -- city p50 0.50 ->
-        // 0.28 ms, metro p50 1.04 -> 1.01 ms over 100 seeded queries
-        // (profiles/r02_latency_kernels.jsonl); larger graphs (country) FRONTIER
-        else if (h->mode == EAT_MODE_REPLICATED && pick_cluster(h, 16, 1)) k = EAT_KERNEL_CLUSTER;
+        // graphs whose whole index (e[], type ranges, headers, cluster bases)
+        // fits the shared memory of a 16-CTA cluster: the asynchronous cluster
+        // kernel -- city p50 0.50 -> 0.24 ms over 100 seeded queries
+        // (profiles/r02_latency_kernels.jsonl)
+        else if (h->mode == EAT_MODE_REPLICATED && pick_cluster(h, 16, 2)) k = EAT_KERNEL_CLUSTER;
+        // else the barrier-free grid kernel (metro p50 1.04 -> ~0.7 ms, country
+        // s0 2.09 -> ~1.1 ms vs FRONTIER; r02_gasync_*.jsonl)
+        else if (h->mode == EAT_MODE_REPLICATED && pick_gasync(h)) k = EAT_KERNEL_GRID_ASYNC;
         else k = EAT_KERNEL_FRONTIER;
     }
     else if (k == EAT_KERNEL_FRONTIER)
@@ -628,7 +613,7 @@ eat_status enqueue_single(eat_handle *h, uint32_t s, uint32_t t_s, uint32_t *d_o
         cix.window = h->cluster_window;
         CUDA_TRY(eat::launch_query_cluster(cix, a, st));
     } else if (h->kernel == EAT_KERNEL_GRID_ASYNC) {
-        eat::GAsyncWork w{h->gw.arr, h->gw.bm, h->d_gacnt, h->gw.ctl, h->gasync_stage, h->gasync_tl};
+        eat::GAsyncWork w{h->gw.arr, h->gw.bm, h->d_gacnt, h->gw.ctl};
         CUDA_TRY(eat::launch_query_gasync(h->ix, w, s, t_s, d_out, st));
         CUDA_TRY(cudaMemcpyAsync(h->d_sweeps1, h->gw.ctl + 8, 4, cudaMemcpyDeviceToDevice, st));
     } else if (h->kernel == EAT_KERNEL_ASYNC) {

@@ -45,25 +45,21 @@ __device__ __forceinline__ void ldg_crec_ga(const DevIndex &ix, uint32_t r, uint
                  : "l"(p + 1));
 }
 
-// STAGE 2: the 16-byte headers and cluster bases of the owned vertices'
-// types are also staged in shared memory (when they fit: metro), so a
-// relaxation's only index access off chip is its hour-cluster record.
 constexpr int kGaThreads = 1024;  // one CTA per SM (512 x 2 ... 256 x 8 within +-3 %: r02_gasync_shape.jsonl)
 constexpr uint32_t kGaWarps = kGaThreads / 32;
 
-template <int STAGE>
+// (Also staging the owned types' headers in shared memory when they fit
+// (metro), or counting marks against credits pre-added to S instead of one
+// returning atomic per marking warp, measured no faster / 8 % slower:
+// r02_gasync_stage.jsonl, r02_ab_gasync_credits.jsonl.)
 __global__ void __launch_bounds__(kGaThreads, 1)
-    k_query_gasync(DevIndex ix, GAsyncWork w, uint32_t s, uint32_t ts, uint32_t *__restrict__ out, uint32_t tl_cap) {
+    k_query_gasync(DevIndex ix, GAsyncWork w, uint32_t s, uint32_t ts, uint32_t *__restrict__ out) {
     extern __shared__ uint4 sm4[];
     const uint32_t n = ix.n, G = gridDim.x, c = blockIdx.x;
     const uint32_t W = (n + 31u) / 32u;
     const uint32_t Wl = (W + G - 1u) / G;                      // words owned by this CTA (some may be >= W)
-    // layout: hdr_s[tl_cap] | rng[32 Wl] | list[32 Wl] | cb_s[tl_cap] | wst[Wl]
-    uint4 *hdr_s = sm4;                                                          // STAGE 2
-    uint2 *rng = reinterpret_cast<uint2 *>(sm4 + (STAGE == 2 ? tl_cap : 0u));   // type range of every owned vertex
-    uint32_t *list = reinterpret_cast<uint32_t *>(rng + Wl * 32u);               // taken vertices
-    uint32_t *cb_s = list + Wl * 32u;                                            // STAGE 2
-    uint32_t *wst = cb_s + (STAGE == 2 ? tl_cap : 0u);                           // STAGE 2: local start per word
+    uint2 *rng = reinterpret_cast<uint2 *>(sm4);               // [32 Wl] type range of every owned vertex
+    uint32_t *list = reinterpret_cast<uint32_t *>(rng + Wl * 32u);  // [32 Wl] taken vertices
     __shared__ uint32_t s_cnt[2];
     __shared__ uint32_t s_done;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
@@ -73,49 +69,12 @@ __global__ void __launch_bounds__(kGaThreads, 1)
     uint32_t *myS = w.cnt + c * kGaCntStride, *myR = myS + 1;
 
     // ---- stage the owned vertices' index; initialize (Alg. 2)
-    auto wrange = [&](uint32_t lw, uint32_t &g0, uint32_t &g1) {  // global type range of owned word lw
-        const uint32_t gw = lw * G + c;
-        g0 = __ldg(ix.type_ptr + min(32u * gw, n));
-        g1 = __ldg(ix.type_ptr + min(32u * gw + 32u, n));
-    };
-    if (STAGE == 2) {
-        if (wid == 0) {  // local start of each owned word's types
-            const uint32_t per = (Wl + 31u) / 32u, lo = min(Wl, lane * per), hi = min(Wl, lo + per);
-            uint32_t sum = 0, g0, g1;
-            for (uint32_t lw = lo; lw < hi; ++lw) {
-                wrange(lw, g0, g1);
-                sum += g1 - g0;
-            }
-            uint32_t incl = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= uint32_t(o)) incl += y;
-            }
-            uint32_t run = incl - sum;
-            for (uint32_t lw = lo; lw < hi; ++lw) {
-                wrange(lw, g0, g1);
-                wst[lw] = run;
-                run += g1 - g0;
-            }
-        }
-        __syncthreads();
-        for (uint32_t lw = wid; lw < Wl; lw += kGaWarps) {  // a warp per owned word
-            uint32_t g0, g1;
-            wrange(lw, g0, g1);
-            for (uint32_t t = g0 + lane; t < g1; t += 32u) {
-                hdr_s[wst[lw] + t - g0] = __ldg(ix.type_hdr + t);
-                cb_s[wst[lw] + t - g0] = __ldg(ix.type_cb + t);
-            }
-        }
-    }
     for (uint32_t li = tid; li < Wl * 32u; li += kGaThreads) {
         const uint32_t gw = (li >> 5) * G + c, v = gw * 32u + (li & 31u);
         uint2 r = make_uint2(0u, 0u);
         if (v < n) {
             const uint32_t a = __ldg(ix.type_ptr + v);
             r = make_uint2(a, __ldg(ix.type_ptr + v + 1) - a);
-            if (STAGE == 2) r.x = wst[li >> 5] + (a - __ldg(ix.type_ptr + 32u * gw));  // local type index
         }
         rng[li] = r;
     }
@@ -211,17 +170,9 @@ __global__ void __launch_bounds__(kGaThreads, 1)
                 if (qp < tot) {
                     const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
                     const uint32_t eu = __ldcg(w.arr + u);
-                    uint32_t cb;
-                    TypeRec tr;
-                    if (STAGE == 2) {  // t is a local type index
-                        cb = cb_s[t];
-                        const uint4 h = hdr_s[t];
-                        tr = TypeRec{h.x, h.y, h.z, h.w};
-                    } else {
-                        cb = __ldg(ix.type_cb + t);
-                        tr = load_type(ix, t);
-                        tr.last |= cb & ix.zero;
-                    }
+                    const uint32_t cb = __ldg(ix.type_cb + t);
+                    TypeRec tr = load_type(ix, t);
+                    tr.last |= cb & ix.zero;
                     if (eu <= tr.last) {
                         uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = r0;
                         const uint32_t kc = cluster_of(ix, eu);
@@ -264,50 +215,42 @@ __global__ void __launch_bounds__(kGaThreads, 1)
     }
 }
 
-size_t gasync_smem(uint32_t n, int G, int stage, uint32_t tl_cap) {
+size_t gasync_smem(uint32_t n, int G) {
     const size_t W = (n + 31u) / 32u, Wl = (W + size_t(G) - 1u) / size_t(G);
-    size_t b = Wl * 32u * (8u + 4u);
-    if (stage == 2) b += size_t(tl_cap) * 20u + Wl * 4u;
-    return b;
+    return Wl * 32u * (8u + 4u);
 }
 
-template <int STAGE>
-int gasync_grid_t(uint32_t n, uint32_t tl_cap) {
-    auto kern = k_query_gasync<STAGE>;
+}  // namespace
+
+int gasync_grid(uint32_t n) {
     int dev = 0, sms = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 0;
-    const size_t smem = gasync_smem(n, sms, STAGE, tl_cap);
+    if (cudaFuncGetAttributes(&fa, k_query_gasync) != cudaSuccess) return 0;
+    const size_t smem = gasync_smem(n, sms);
     if (smem + fa.sharedSizeBytes > size_t(optin)) return 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 0;
+    if (cudaFuncSetAttribute(k_query_gasync, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+        return 0;
     int per_sm = 0;  // every CTA must be resident (they wait on each other): one per SM
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGaThreads, smem) != cudaSuccess || per_sm < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_gasync, kGaThreads, smem) != cudaSuccess ||
+        per_sm < 1)
         return 0;
     return sms;
 }
 
-}  // namespace
-
-int gasync_grid(uint32_t n, int stage, uint32_t tl_cap) {
-    return stage == 2 ? gasync_grid_t<2>(n, tl_cap) : gasync_grid_t<1>(n, 0);
-}
-
 cudaError_t launch_query_gasync(const DevIndex &ix, const GAsyncWork &w, uint32_t s, uint32_t t_s, uint32_t *d_out,
                                 cudaStream_t st) {
-    const int G = gasync_grid(ix.n, w.stage, w.tl_cap);
+    const int G = gasync_grid(ix.n);
     if (G < 1) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaMemsetAsync(w.ctl + kBarWord, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     DevIndex ixc = ix;
     GAsyncWork wc = w;
-    uint32_t tl = w.tl_cap;
-    void *args[] = {&ixc, &wc, &s, &t_s, &d_out, &tl};
-    const void *kern = w.stage == 2 ? (const void *)k_query_gasync<2> : (const void *)k_query_gasync<1>;
-    return cudaLaunchCooperativeKernel(kern, dim3(unsigned(G)), dim3(kGaThreads), args,
-                                       gasync_smem(ix.n, G, w.stage, w.tl_cap), st);
+    void *args[] = {&ixc, &wc, &s, &t_s, &d_out};
+    return cudaLaunchCooperativeKernel((const void *)k_query_gasync, dim3(unsigned(G)), dim3(kGaThreads), args,
+                                       gasync_smem(ix.n, G), st);
 }
 
 }  // namespace eat

@@ -145,11 +145,9 @@ struct GAsyncWork {
     uint32_t *bm;    // [W] marked-vertex bitmap
     uint32_t *cnt;   // [32 * grid] per-CTA counters: S (marks set), R (vertices done)
     uint32_t *ctl;   // [kCtlWords]: 0 done flag, 8 iterations of CTA 0, kBarWord grid barrier
-    int stage;       // 1: type ranges staged in shared memory; 2: + headers and cluster bases
-    uint32_t tl_cap; // stage 2: most types owned by one CTA
 };
-// CTAs of the launch for n vertices at a staging level (one per SM; 0 if it does not fit shared memory).
-int gasync_grid(uint32_t n, int stage, uint32_t tl_cap);
+// CTAs of the launch for n vertices (one per SM; 0 if the per-CTA slices do not fit shared memory).
+int gasync_grid(uint32_t n);
 cudaError_t launch_query_gasync(const DevIndex &ix, const GAsyncWork &w, uint32_t s, uint32_t t_s, uint32_t *d_out,
                                 cudaStream_t st);
 

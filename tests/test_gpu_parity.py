@@ -230,7 +230,7 @@ def test_metro_single_query():
     """BASELINE configs[3]: metro network, global e[] (frontier kernel)."""
     tt = synth.generate("metro")
     eng = Engine.from_timetable(tt)
-    assert eng.stats()["kernel_name"] in ("frontier", "cta", "async", "cluster")
+    assert eng.stats()["kernel_name"] in ("frontier", "cta", "async", "cluster", "grid_async")
     csa = oracle.CSA(tt.num_vertices, *tt.arrays())
     for s, t_s in [synth.SINGLE_QUERY, (777, 30000)]:
         _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"metro ({s},{t_s})")
