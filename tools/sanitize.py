@@ -32,6 +32,9 @@ CASES = {
     "cluster16": ("k_query_cluster<2> (16 CTAs, DSMEM e[], staged index)", dict(kernel="cluster", cluster_ctas=16),
                   "single"),
     "cluster2": ("k_query_cluster (2 CTAs)", dict(kernel="cluster", cluster_ctas=2, window=600), "single"),
+    "cluster_sync": ("k_query_cluster<.., sync> (4 CTAs, cluster barrier per sweep)",
+                     dict(kernel="cluster", cluster_ctas=4, cluster_sync=True), "single"),
+    "grid_async": ("k_query_gasync (barrier-free grid, per-CTA counters)", dict(kernel="grid_async"), "single"),
     "grid_frontier": ("k_query_grid<32, frontier>", dict(kernel="frontier"), "single"),
     "grid_flat": ("k_query_grid<32, flat> (subwarp 64)", dict(kernel="frontier", subwarp=64), "single"),
     "grid_full": ("k_query_grid<1, full sweep>", dict(kernel="full_sweep"), "single"),
