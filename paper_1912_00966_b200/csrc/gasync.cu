@@ -45,6 +45,10 @@ __device__ __forceinline__ void ldg_crec_ga(const DevIndex &ix, uint32_t r, uint
                  : "l"(p + 1));
 }
 
+#ifndef EAT_GA_CONT
+#define EAT_GA_CONT 1  // continuation: a warp relaxes the vertices it just lowered (one level): metro -5 %, country -2 %, r02_ab_gasync_cont.jsonl
+#endif
+
 constexpr int kGaThreads = 1024;  // one CTA per SM (512 x 2 ... 256 x 8 within +-3 %: r02_gasync_shape.jsonl)
 constexpr uint32_t kGaWarps = kGaThreads / 32;
 
@@ -95,6 +99,33 @@ __global__ void __launch_bounds__(kGaThreads, 1)
         atomicAdd(w.cnt + ((si >> 5) % G) * kGaCntStride, 1u);  // the source's mark, counted by its owner
     }
     grid_sync(bar, bar_epoch, G);
+
+    // relax type t of a source with arrival eu; returns the target it lowered
+    auto relax = [&](uint32_t eu, uint32_t t) -> uint32_t {
+        const uint32_t cb = __ldg(ix.type_cb + t);
+        TypeRec tr = load_type(ix, t);
+        tr.last |= cb & ix.zero;
+        if (eu > tr.last) return kNone;
+        uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = r0;
+        const uint32_t kc = cluster_of(ix, eu);
+        if (eu > tr.first) ldg_crec_ga(ix, cb + kc, r0, r1);  // overlaps the e[v] read
+        const uint32_t av = __ldcg(w.arr + tr.v);
+        if (max(eu, tr.first) + tr.lam >= av) return kNone;
+        const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan(ix, r0, r1, kc, eu);
+        const uint32_t cand = tc + tr.lam;
+        return (cand < av && cand < atomicMin(w.arr + tr.v, cand)) ? tr.v : kNone;
+    };
+    // mark the lanes' lowered vertices (wm: ballot of mv != kNone; warp-uniform)
+    auto mark = [&](uint32_t mv, uint32_t wm) {
+        if (!wm) return;
+        // counted in S (returning atomic: performed) before any bit is set
+        if (lane == uint32_t(__ffs(wm) - 1)) atomicAdd(myS, uint32_t(__popc(wm)));
+        __syncwarp();
+        uint32_t dup = 0;
+        if (mv != kNone) dup = atomicOr(w.bm + (mv >> 5), 1u << (mv & 31u)) & (1u << (mv & 31u));
+        const uint32_t dm = __ballot_sync(0xFFFFFFFFu, dup != 0u);
+        if (dm && lane == uint32_t(__ffs(dm) - 1)) atomicSub(myS, uint32_t(__popc(dm)));
+    };
 
     uint32_t iters = 0;
     for (;;) {
@@ -167,34 +198,45 @@ __global__ void __launch_bounds__(kGaThreads, 1)
                 const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
                 const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
                 uint32_t mv = kNone;  // vertex this lane lowered (to be marked)
-                if (qp < tot) {
-                    const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
-                    const uint32_t eu = __ldcg(w.arr + u);
-                    const uint32_t cb = __ldg(ix.type_cb + t);
-                    TypeRec tr = load_type(ix, t);
-                    tr.last |= cb & ix.zero;
-                    if (eu <= tr.last) {
-                        uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = r0;
-                        const uint32_t kc = cluster_of(ix, eu);
-                        if (eu > tr.first) ldg_crec_ga(ix, cb + kc, r0, r1);  // overlaps the e[v] read
-                        const uint32_t av = __ldcg(w.arr + tr.v);
-                        if (max(eu, tr.first) + tr.lam < av) {
-                            const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan(ix, r0, r1, kc, eu);
-                            const uint32_t cand = tc + tr.lam;
-                            if (cand < av && cand < atomicMin(w.arr + tr.v, cand)) mv = tr.v;
-                        }
-                    }
-                }
-                const uint32_t wm = __ballot_sync(0xFFFFFFFFu, mv != kNone);
+                if (qp < tot) mv = relax(__ldcg(w.arr + u), o_p0 + (qp - (o_incl - o_nt)));
+                uint32_t wm = __ballot_sync(0xFFFFFFFFu, mv != kNone);
+#if EAT_GA_CONT
                 if (wm) {
-                    // counted in S (returning atomic: performed) before any bit is set
-                    if (lane == uint32_t(__ffs(wm) - 1)) atomicAdd(myS, uint32_t(__popc(wm)));
-                    __syncwarp();
-                    uint32_t dup = 0;
-                    if (mv != kNone) dup = atomicOr(w.bm + (mv >> 5), 1u << (mv & 31u)) & (1u << (mv & 31u));
-                    const uint32_t dm = __ballot_sync(0xFFFFFFFFu, dup != 0u);
-                    if (dm && lane == uint32_t(__ffs(dm) - 1)) atomicSub(myS, uint32_t(__popc(dm)));
+                    // continuation: the vertices this warp just lowered are relaxed by
+                    // the warp at once (one level), instead of marked for their owners
+                    uint32_t cp0 = 0, cnt = 0;
+                    if (mv != kNone) {
+                        cp0 = __ldg(ix.type_ptr + mv);
+                        cnt = __ldg(ix.type_ptr + mv + 1) - cp0;
+                    }
+                    uint32_t cin = cnt;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, cin, o);
+                        if (lane >= uint32_t(o)) cin += y;
+                    }
+                    const uint32_t ctot = __shfl_sync(0xFFFFFFFFu, cin, 31);
+                    const uint32_t cx = mv;
+                    for (uint32_t cbase = 0; cbase < ctot; cbase += 32u) {
+                        const uint32_t cq = cbase + lane;
+                        uint32_t L2 = 0;
+#pragma unroll
+                        for (uint32_t step = 16; step > 0; step >>= 1) {
+                            const uint32_t v = __shfl_sync(0xFFFFFFFFu, cin, L2 + step - 1u);
+                            if (v <= cq) L2 += step;
+                        }
+                        const uint32_t c_incl = __shfl_sync(0xFFFFFFFFu, cin, L2);
+                        const uint32_t c_nt = __shfl_sync(0xFFFFFFFFu, cnt, L2);
+                        const uint32_t c_p0 = __shfl_sync(0xFFFFFFFFu, cp0, L2);
+                        const uint32_t cu = __shfl_sync(0xFFFFFFFFu, cx, L2);
+                        uint32_t mv2 = kNone;
+                        if (cq < ctot) mv2 = relax(__ldcg(w.arr + cu), c_p0 + (cq - (c_incl - c_nt)));
+                        mark(mv2, __ballot_sync(0xFFFFFFFFu, mv2 != kNone));
+                    }
+                    wm = 0;
                 }
+#endif
+                mark(mv, wm);
             }
         }
         __syncthreads();  // every relaxation (and its mark count) of the F taken vertices is done
