@@ -422,7 +422,10 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                         }
                     }
                     // (a segmented min over lanes sharing the target before the
-                    // shared atomicMin costs 10 %: r02_ab_type_hdr16_segmin.jsonl)
+                    // shared atomicMin costs 10 %: r02_ab_type_hdr16_segmin.jsonl;
+                    // relaxing a target lowered within the window at once instead
+                    // of marking it -- continuation -- halves the sweeps but costs
+                    // 11 %: +18 % type evaluations, r02_ab_cta_continuation.jsonl)
                     const uint32_t cand = tc + tr.lam;
                     if (cand < av) {
                         const uint32_t old = ar.amin(tr.v, cand, &s_ovf);
