@@ -452,9 +452,10 @@ def _batch_roofline(tt, src, ts, dev, stream, args, step_ms, st0):
         mean_launch_s = (sum(step_ms) / len(step_ms)) / 1e3
         achieved = cnt["algorithmic_bytes"] / mean_launch_s / 1e9
         l2 = _probe_l2_gbs(dev, stream)
-        traffic, ncu_src = None, None
+        traffic, ncu_src, tj = None, None, {}
         tp = os.path.join(ROOT, "profiles", "traffic_city_batch.json")
-        if os.path.exists(tp):
+        tp_ok = os.path.exists(tp)
+        if tp_ok:
             with open(tp) as f:
                 tj = json.load(f)
             traffic, ncu_src = tj.get("dram_bytes_per_launch"), tj.get("source")
@@ -469,7 +470,13 @@ def _batch_roofline(tt, src, ts, dev, stream, args, step_ms, st0):
                 "hbm": {"peak": hbm, "peak_source": hbm_src, "frac_of_algorithmic": achieved / hbm,
                         "dram_gbs": (traffic / mean_launch_s / 1e9) if traffic else None,
                         "dram_frac": (traffic / mean_launch_s / 1e9 / hbm) if traffic else None,
-                        "traffic_source": ncu_src}}
+                        "traffic_source": ncu_src},
+                # what actually bounds it: instruction issue -- the
+                # committed ncu capture's issue-slot utilisation and IPC of 4
+                "issue": {"issue_active_frac": (tj.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0) / 100.0)
+                          if tp_ok else None,
+                          "warp_instructions_per_query": (tj.get("warp_instructions", 0) / 1e4) if tp_ok else None,
+                          "source": ncu_src}}
     except Exception as exc:  # keep the bench line even if accounting fails
         return {"bound": "l2", "achieved": None, "peak": None, "unit": "GB/s", "frac": None, "traffic": None,
                 "error": repr(exc)}
