@@ -375,7 +375,9 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                 const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
                 // (measured alternatives, profiles/r02_ab_owner_search_variants.jsonl:
                 // a start-bitmask + shared-memory owner map -1 %, e[u] read once per
-                // chunk and shuffled -2 %: the per-pair read sees fresher arrivals)
+                // chunk and shuffled -2 %: the per-pair read sees fresher arrivals;
+                // scan and search over the first 2^ceil(log2 g) lanes only -4 %,
+                // r02_ab_cta_pow2_search.jsonl)
                 for (uint32_t base = 0; base < tot; base += 32u) {
                     const uint32_t qp = base + lane;
                     // owner lane: smallest L with incl[L] > qp
