@@ -401,8 +401,10 @@ __global__ void __launch_bounds__(kClThreads, 1)
                                 }
                             }
                         }
-                        // count the marks in CTA 0 before setting them
+                        // (relaxing the lowered vertices at once -- continuation, as in
+                        // gasync.cu -- is 11 % slower here: r02_ab_cluster_continuation.jsonl)
                         const uint32_t wm = __ballot_sync(0xFFFFFFFFu, mv != kNone);
+                        // count the marks in CTA 0 before setting them
                         if (wm) {
                             if (lane == uint32_t(__ffs(wm) - 1)) {
                                 // returns once performed in CTA 0: every mark below is
