@@ -52,7 +52,10 @@ __device__ __forceinline__ void ldg_crec_ga(const DevIndex &ix, uint32_t r, uint
 constexpr int kGaThreads = 1024;  // one CTA per SM (512 x 2 ... 256 x 8 within +-3 %: r02_gasync_shape.jsonl)
 constexpr uint32_t kGaWarps = kGaThreads / 32;
 
-// (Also staging the owned types' headers in shared memory when they fit
+// (A warp-asynchronous variant -- each warp polls and relaxes its own words,
+// no CTA barrier at all -- is 1.7-2.8x slower: 4,736 polling warps and one
+// warp per word of work, r02_ab_gasync_warp.jsonl.  Also staging the owned
+// types' headers in shared memory when they fit
 // (metro), or counting marks against credits pre-added to S instead of one
 // returning atomic per marking warp, measured no faster / 8 % slower:
 // r02_gasync_stage.jsonl, r02_ab_gasync_credits.jsonl.)
