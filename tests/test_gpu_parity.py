@@ -240,6 +240,26 @@ def test_metro_single_query():
             _assert_rows(e2.query(s, t_s), csa.query(s, t_s), f"metro {kernel} ({s},{t_s})")
 
 
+@pytest.mark.parametrize("name,kernel,nq", [("city", "cluster", 300), ("metro", "grid_async", 100),
+                                             ("city", "grid_async", 100)])
+def test_async_kernels_many_queries(name, kernel, nq):
+    """The asynchronous single-query kernels (the bench's AUTO choice for
+    city / metro) on many seeded queries at full size, every stop of every
+    row against the oracle (their termination is timing-dependent: many
+    queries exercise many interleavings)."""
+    tt = synth.generate(name)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    eng = Engine.from_timetable(tt, kernel=kernel, subtrips=3)
+    rng = np.random.default_rng(2024)
+    out = torch.empty(tt.num_vertices, dtype=torch.int32, device="cuda")
+    for i in range(nq):
+        s, t_s = int(rng.integers(tt.num_vertices)), int(rng.integers(0, 2 * 86400))
+        eng.query_device(s, t_s, out)
+        _assert_rows(out.cpu().numpy().view(np.uint32), csa.query(s, t_s), f"{name} {kernel} q{i}=({s},{t_s})")
+    eng.close()
+    csa.close()
+
+
 @pytest.mark.parametrize("ctas", [2, 4, 8, 16])
 def test_cluster_kernel_sizes(ctas):
     """EAT_KERNEL_CLUSTER with every cluster size: e[] spread over 2..16
@@ -535,8 +555,16 @@ def test_country_single_query():
     rng = np.random.default_rng(44)
     qs = [synth.SINGLE_QUERY] + [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 86400))) for _ in range(3)]
     want = [csa.query(*q) for q in qs]
+    # the bench's kernel (AUTO = grid_async here) on 12 more seeded queries
+    more = [(int(rng.integers(tt.num_vertices)), int(rng.integers(0, 2 * 86400))) for _ in range(12)]
+    want_more = [csa.query(*q) for q in more]
     csa.close()
-    for kw in ({"subtrips": 3}, {"subtrips": 3, "kernel": "grid_async"}, {"mode": "edge_partitioned", "part_count": 1},
+    eng = Engine.from_timetable(tt, subtrips=3)
+    assert eng.stats()["kernel_name"] in ("grid_async", "frontier")
+    for q, w in zip(more, want_more):
+        _assert_rows(eng.query(*q), w, f"country auto {q}")
+    eng.close()
+    for kw in ({"subtrips": 3, "kernel": "frontier"}, {"subtrips": 3, "kernel": "grid_async"}, {"mode": "edge_partitioned", "part_count": 1},
                {"mode": "edge_partitioned", "part_count": 2, "subtrips": 3},
                {"mode": "edge_partitioned", "part_count": 2, "exchange": "peer", "subtrips": 3}):
         eng = Engine.from_timetable(tt, **kw)
