@@ -124,9 +124,21 @@ def test_random_small_instances(kernel):
 
 
 def test_edge_cases():
-    # one vertex, no connections
+    # one vertex, no connections (every single-query kernel)
     eng = Engine(1, [], [], [], [])
     assert eng.query(0, 5).tolist() == [5]
+    for kernel in KERNELS:
+        if kernel == "connection":
+            continue
+        e1 = Engine(1, [], [], [], [], kernel=kernel)
+        assert e1.query(0, 5).tolist() == [5], kernel
+        e1.close()
+    # a few vertices, one connection (bitmap words beyond the graph on most CTAs)
+    for kernel in KERNELS:
+        e3 = Engine(3, [0], [2], [10], [5], kernel=kernel)
+        assert e3.query(0, 7).tolist() == [7, INF, 15], kernel
+        assert e3.query(0, 11).tolist() == [11, INF, INF], kernel
+        e3.close()
     # isolated source, late start, t_s = 0, t_s = INF-1
     tt = synth.generate("tiny")
     csa = oracle.CSA(tt.num_vertices, *tt.arrays())
