@@ -272,6 +272,24 @@ def test_async_kernels_many_queries(name, kernel, nq):
     csa.close()
 
 
+@pytest.mark.parametrize("stops,irregular", [(3000, 0.0), (30000, 0.3), (60000, 0.3)])
+def test_auto_single_query_sizes(stops, irregular):
+    """AUTO's single-query choice across graph sizes (cluster kernel with the
+    whole index on chip, cluster with type ranges only, grid-async): every
+    row vs the oracle on seeded queries."""
+    tt = synth.generate("custom", stops=stops, edges=3 * stops, conns=60 * stops, irregular=irregular, seed=stops)
+    csa = oracle.CSA(tt.num_vertices, *tt.arrays())
+    eng = Engine.from_timetable(tt, subtrips=3)
+    st = eng.stats()
+    assert st["kernel_name"] in ("cluster", "grid_async"), st["kernel_name"]
+    rng = np.random.default_rng(stops)
+    for _ in range(12):
+        s, t_s = int(rng.integers(tt.num_vertices)), int(rng.integers(0, 2 * 86400))
+        _assert_rows(eng.query(s, t_s), csa.query(s, t_s), f"{stops} stops {st['kernel_name']} ({s},{t_s})")
+    eng.close()
+    csa.close()
+
+
 @pytest.mark.parametrize("ctas", [2, 4, 8, 16])
 def test_cluster_kernel_sizes(ctas):
     """EAT_KERNEL_CLUSTER with every cluster size: e[] spread over 2..16
