@@ -1006,6 +1006,13 @@ eat_status launch_batch_cta(eat_handle *h, const uint32_t *d_sources, const uint
         a.ovf_list = h->d_ovf[slot] + 1;
         a.ovf_cnt = h->d_ovf[slot];
     }
+    // more queries than resident CTAs: hand them out by departure time (the
+    // expensive ones first, a short last wave; N = 8 share of the city batch
+    // 1.49 -> 1.35 ms, profiles/r02_order_by_time.jsonl)
+    if (h->sort_batches && nq > uint64_t(h->cta_grid)) {
+        CUDA_TRY(eat::sort_queries_by_time(d_times, nq, h->qsort[slot], st));
+        a.qorder = h->qsort[slot].v1;
+    }
     CUDA_TRY(eat::launch_query_cta(h->ix, a, st));
     return EAT_OK;
 }

@@ -889,10 +889,10 @@ cudaError_t launch_cta_one(const DevIndex &ix, const CtaArgs &a, const uint32_t 
 // list (count read on the device; empty in practice for one-day feeds).
 template <bool COUNT, int T, int L>
 cudaError_t launch_cta_pair(const DevIndex &ix, const CtaArgs &a, cudaStream_t st) {
-    if (!a.arr16) return launch_cta_one<COUNT, T, L, false>(ix, a, nullptr, nullptr, nullptr, nullptr, a.grid_cap, st);
+    if (!a.arr16) return launch_cta_one<COUNT, T, L, false>(ix, a, a.qorder, nullptr, nullptr, nullptr, a.grid_cap, st);
     cudaError_t e = cudaMemsetAsync(a.ovf_cnt, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
-    e = launch_cta_one<COUNT, T, L, true>(ix, a, nullptr, nullptr, a.ovf_list, a.ovf_cnt, a.grid_cap, st);
+    e = launch_cta_one<COUNT, T, L, true>(ix, a, a.qorder, nullptr, a.ovf_list, a.ovf_cnt, a.grid_cap, st);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -1069,6 +1069,35 @@ cudaError_t sort_queries_by_source(const DevIndex &ix, const uint32_t *src, uint
     while (bits < 32 && (1ull << bits) <= ix.n) ++bits;
     size_t tmp = sc.tmp_bytes;
     return cub::DeviceRadixSort::SortPairs(sc.tmp, tmp, sc.k0, sc.k1, sc.v0, sc.v1, int(nq), 0, bits, st);
+}
+
+namespace {
+__global__ void k_iota(uint32_t *v, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        v[i] = uint32_t(i);
+}
+}  // namespace
+
+cudaError_t sort_queries_by_time(const uint32_t *ts, uint64_t nq, SortScratch &sc, cudaStream_t st) {
+    if (nq > 0xFFFFFFFFull) return cudaErrorInvalidValue;
+    cudaError_t e;
+    if (sc.cap < nq) {
+        sort_scratch_free(sc);
+        size_t tmp = 0;
+        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                                 (uint32_t *)nullptr, (uint32_t *)nullptr, int(nq))) != cudaSuccess)
+            return e;
+        void **bufs[] = {(void **)&sc.k0, (void **)&sc.k1, (void **)&sc.v0, (void **)&sc.v1};
+        for (void **b : bufs)
+            if ((e = cudaMalloc(b, nq * 4)) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&sc.tmp, tmp)) != cudaSuccess) return e;
+        sc.tmp_bytes = tmp;
+        sc.cap = nq;
+    }
+    k_iota<<<unsigned(std::min<uint64_t>((nq + 255) / 256, 1184)), 256, 0, st>>>(sc.v0, nq);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    size_t tmp = sc.tmp_bytes;
+    return cub::DeviceRadixSort::SortPairs(sc.tmp, tmp, ts, sc.k1, sc.v0, sc.v1, int(nq), 0, 32, st);
 }
 
 void sort_scratch_free(SortScratch &sc) {

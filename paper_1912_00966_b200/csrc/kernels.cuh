@@ -81,7 +81,8 @@ struct CtaArgs {
     uint32_t *ovf_list = nullptr;   // [nq] + 1 count word (ovf_cnt): uint16-pass overflow queries
     uint32_t *ovf_cnt = nullptr;
     unsigned int *done = nullptr;   // streamed e2e: [nq] finished-row flags (mapped host memory) or NULL
-    int threads = 256;              // 1024, 512, 384, 256, 192 or 128
+    const uint32_t *qorder = nullptr;  // optional [nq]: the order in which CTAs take the queries
+    int threads = 256;              // 1024, 512, 384, 320, 256, 192 or 128
     bool arr16 = false;             // uint16 pass (+ uint32 recompute of overflowing queries)
     uint64_t grid_cap = 0;
 };
@@ -117,6 +118,11 @@ struct SortScratch {
 cudaError_t sort_queries_by_source(const DevIndex &ix, const uint32_t *src, uint64_t nq, SortScratch &sc,
                                    cudaStream_t st);
 void sort_scratch_free(SortScratch &sc);
+// Query order by departure time (batched CTA kernel): v1[i] = the i-th query
+// when sorted by t_s ascending -- a later departure reaches less of the day's
+// service and is cheaper (city: 21-24 h 3x cheaper), so expensive queries go
+// first and the last wave of the persistent grid is short.
+cudaError_t sort_queries_by_time(const uint32_t *ts, uint64_t nq, SortScratch &sc, cudaStream_t st);
 
 // Arguments of the cluster kernel (cluster.cu: one query per thread-block
 // cluster, e[] distributed over the CTAs' shared memory).
