@@ -1009,8 +1009,13 @@ eat_status launch_batch_cta(eat_handle *h, const uint32_t *d_sources, const uint
     // more queries than resident CTAs: hand them out by departure time (the
     // expensive ones first, a short last wave; N = 8 share of the city batch
     // 1.49 -> 1.35 ms, profiles/r02_order_by_time.jsonl)
-    if (h->sort_batches && nq > uint64_t(h->cta_grid)) {
-        CUDA_TRY(eat::sort_queries_by_time(d_times, nq, h->qsort[slot], st));
+    // Not for the direct e2e launch (slot 1), whose rows cross PCIe as the
+    // queries finish: cheap queries last would finish in a burst at the end and
+    // their rows would queue on the link (e2e 1.106M -> 0.99M q/s, also with
+    // coarse time buckets: profiles/r02_order_by_time_e2e.jsonl); in caller
+    // order the row traffic is spread over the whole launch.
+    if (h->sort_batches && nq > uint64_t(h->cta_grid) && slot != 1) {
+        CUDA_TRY(eat::sort_queries_by_time(d_times, nq, 0, h->qsort[slot], st));
         a.qorder = h->qsort[slot].v1;
     }
     CUDA_TRY(eat::launch_query_cta(h->ix, a, st));

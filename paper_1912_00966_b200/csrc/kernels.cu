@@ -1072,13 +1072,17 @@ cudaError_t sort_queries_by_source(const DevIndex &ix, const uint32_t *src, uint
 }
 
 namespace {
-__global__ void k_iota(uint32_t *v, uint64_t n) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+// keys = t_s >> shift (coarse buckets keep the caller order inside each --
+// the radix sort is stable), values = query index
+__global__ void k_time_keys(const uint32_t *ts, uint64_t n, uint32_t shift, uint32_t *k, uint32_t *v) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        k[i] = ts[i] >> shift;
         v[i] = uint32_t(i);
+    }
 }
 }  // namespace
 
-cudaError_t sort_queries_by_time(const uint32_t *ts, uint64_t nq, SortScratch &sc, cudaStream_t st) {
+cudaError_t sort_queries_by_time(const uint32_t *ts, uint64_t nq, uint32_t shift, SortScratch &sc, cudaStream_t st) {
     if (nq > 0xFFFFFFFFull) return cudaErrorInvalidValue;
     cudaError_t e;
     if (sc.cap < nq) {
@@ -1094,10 +1098,10 @@ cudaError_t sort_queries_by_time(const uint32_t *ts, uint64_t nq, SortScratch &s
         sc.tmp_bytes = tmp;
         sc.cap = nq;
     }
-    k_iota<<<unsigned(std::min<uint64_t>((nq + 255) / 256, 1184)), 256, 0, st>>>(sc.v0, nq);
+    k_time_keys<<<unsigned(std::min<uint64_t>((nq + 255) / 256, 1184)), 256, 0, st>>>(ts, nq, shift, sc.k0, sc.v0);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     size_t tmp = sc.tmp_bytes;
-    return cub::DeviceRadixSort::SortPairs(sc.tmp, tmp, ts, sc.k1, sc.v0, sc.v1, int(nq), 0, 32, st);
+    return cub::DeviceRadixSort::SortPairs(sc.tmp, tmp, sc.k0, sc.k1, sc.v0, sc.v1, int(nq), 0, int(32 - shift), st);
 }
 
 void sort_scratch_free(SortScratch &sc) {

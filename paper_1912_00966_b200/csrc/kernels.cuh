@@ -122,7 +122,8 @@ void sort_scratch_free(SortScratch &sc);
 // when sorted by t_s ascending -- a later departure reaches less of the day's
 // service and is cheaper (city: 21-24 h 3x cheaper), so expensive queries go
 // first and the last wave of the persistent grid is short.
-cudaError_t sort_queries_by_time(const uint32_t *ts, uint64_t nq, SortScratch &sc, cudaStream_t st);
+// shift: sort by t_s >> shift (stable: caller order inside each bucket).
+cudaError_t sort_queries_by_time(const uint32_t *ts, uint64_t nq, uint32_t shift, SortScratch &sc, cudaStream_t st);
 
 // Arguments of the cluster kernel (cluster.cu: one query per thread-block
 // cluster, e[] distributed over the CTAs' shared memory).
