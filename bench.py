@@ -645,7 +645,11 @@ def run_gpu(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(NQ * 8),
                     "d2h_bytes_per_step": int(NQ * tt.num_vertices * 4), "host_buffers": "pinned",
                     "rows_match_device_run": e2e_ok},
-            "gpu_launches": args.steps,
+            # per step: the batched kernel, plus (more queries than resident
+            # CTAs) the departure-time hand-out order -- our key kernel and the
+            # 5 launches of cub's radix sort compiled into libeat
+            "gpu_launches": args.steps * (2 if (st0["cta_grid"] > 0 and nq > st0["cta_grid"]) else 1),
+            "library_launches": args.steps * (5 if (st0["cta_grid"] > 0 and nq > st0["cta_grid"]) else 0),
             "clocks": clk,
             "roofline": roof,
             "cpu_baseline": cpu,
