@@ -307,7 +307,10 @@ eat_status eat_get_stats(const eat_handle *h, eat_stats *out);
 /* Device self-test of the exactness assumptions behind two integer shortcuts
  * of the kernels: (1) Algorithm 6's ceil-division ceil((e - start) / diff)
  * computed in fp32 without integer fix-up, for every pair of
- * 12-bit operands; (2) the hour cluster k = floor(e / cluster_seconds)
+ * 12-bit operands (and 0 for a zero numerator), with the branch-free item
+ * lookup of the single-query kernels checked against the branching one
+ * (every first-term/difference pair, four run lengths, the boundary bounds);
+ * (2) the hour cluster k = floor(e / cluster_seconds)
  * computed by reciprocal multiplication with this handle's
  * cluster width, for every e < 2^31.  failures[0], failures[1] receive the
  * mismatch counts (0 on a correct device).  Errors: EAT_EINVAL (NULL),

@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
                                 const uint32_t ea = e_addr(tr.v);
                                 const uint32_t av = cl_ld(ea);
                                 if (max(eu, tr.first) + tr.lam < av) {
-                                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan(ix, r0, r1, kc, eu);
+                                    const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan<true>(ix, r0, r1, kc, eu);
                                     const uint32_t cand = tc + tr.lam;
                                     if (cand < av && cand < cl_min(ea, cand)) mv = tr.v;
                                 }

@@ -41,6 +41,16 @@ __device__ __forceinline__ uint32_t item_next(uint32_t it, uint32_t x) {
     return off + ceil_div12(x - off, stride) * stride;
 }
 
+// item_next without branches: x <= off gives a = 0, whose ceil-division is 0
+// (also for a singleton's stride 0: (0 - 0.5) * rcp(0) = -inf -> 0); the
+// result is kept only for a non-empty item with x <= last.
+__device__ __forceinline__ uint32_t item_next_bf(uint32_t it, uint32_t x) {
+    const uint32_t off = it & 0xFFFu, stride = (it >> 12) & 0xFFFu, cm1 = it >> 24;
+    const uint32_t a = x > off ? x - off : 0u;
+    const uint32_t r = off + ceil_div12(a, stride) * stride;
+    return (it != kItemEmpty && x <= off + cm1 * stride) ? r : kNone;
+}
+
 // Hour cluster of time e (k = e[u]/3600): exact reciprocal
 // multiply, valid for e < 2^31 (every finite time): the product error is
 // below 2^-l <= 1/cs, so the floor is exact.
@@ -52,6 +62,12 @@ __device__ __forceinline__ uint32_t cluster_of(const DevIndex &ix, uint32_t e) {
 // given the cluster's 32-byte record (r0, r1): smallest term >= eu among the
 // cluster's APs, else the first departure of the next non-empty cluster
 // (precomputed as next_min).  Precondition: first < eu <= last.
+// LAT (latency-bound single-query kernels): items 0 and 1 -- most slots hold
+// one or two -- are evaluated without branches and the rest only if item 1
+// starts before x (city / metro single query -2 % / -3 %); the throughput-
+// bound batched kernel keeps the early exits (its instruction count decides:
+// -0.5 % with LAT, profiles/r02_ab_scan_lat.jsonl).
+template <bool LAT = false>
 __device__ __forceinline__ uint32_t cluster_scan(const DevIndex &ix, const uint4 &r0, const uint4 &r1, uint32_t k,
                                                  uint32_t eu) {
     const uint32_t x = eu - k * ix.cs;
@@ -61,6 +77,17 @@ __device__ __forceinline__ uint32_t cluster_scan(const DevIndex &ix, const uint4
             const uint32_t it = __ldg(ix.pool + r0.z + i);
             best = min(best, item_next(it, x));
             if ((it & 0xFFFu) >= x) break;  // items sorted by first term: later ones start later
+        }
+    } else if (LAT) {
+        best = min(item_next_bf(r0.y, x), item_next_bf(r0.z, x));
+        if (r0.w != kItemEmpty && (r0.z & 0xFFFu) < x) {
+            const uint32_t items[kInlineItems - 2] = {r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+            for (int i = 0; i < kInlineItems - 2; ++i) {
+                if (items[i] == kItemEmpty) break;  // slots are filled from the front
+                best = min(best, item_next(items[i], x));
+                if ((items[i] & 0xFFFu) >= x) break;
+            }
         }
     } else {
         const uint32_t items[kInlineItems] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kGaThreads, 1)
         if (eu > tr.first) ldg_crec_ga(ix, cb + kc, r0, r1);  // overlaps the e[v] read
         const uint32_t av = __ldcg(w.arr + tr.v);
         if (max(eu, tr.first) + tr.lam >= av) return kNone;
-        const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan(ix, r0, r1, kc, eu);
+        const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan<true>(ix, r0, r1, kc, eu);
         const uint32_t cand = tc + tr.lam;
         return (cand < av && cand < atomicMin(w.arr + tr.v, cand)) ? tr.v : kNone;
     };

@@ -1112,15 +1112,32 @@ void sort_scratch_free(SortScratch &sc) {
 }
 
 namespace {
-// eat_selftest: (1) ceil_div12 == integer ceil for every 1 <= a, s < 2^12;
+// eat_selftest: (1) ceil_div12 == integer ceil for every 1 <= a, s < 2^12,
+// and 0 for a = 0 (every s, also 0); the branch-free item_next_bf ==
+// item_next for every (first-term offset, difference) pair with count - 1 in
+// {0, 1, 7, 255} at x = 0, off - 1, off, off + 1, off + stride, last,
+// last + 1, 4095, and for the empty item;
 // (2) cluster_of(e) == e / cs for every e < 2^31 (this index's cs).
 __global__ void k_selftest(DevIndex ix, unsigned long long *fail) {
     const uint64_t gtid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x, gsz = uint64_t(gridDim.x) * blockDim.x;
     unsigned long long f0 = 0, f1 = 0;
     for (uint64_t i = gtid; i < (1ull << 24); i += gsz) {
         const uint32_t a = uint32_t(i >> 12), st = uint32_t(i & 0xFFFu);
-        if (a == 0 || st == 0) continue;
-        if (ceil_div12(a, st) != (a + st - 1u) / st) ++f0;
+        if (a == 0) {
+            if (ceil_div12(0u, st) != 0u) ++f0;
+        } else if (st != 0 && ceil_div12(a, st) != (a + st - 1u) / st) {
+            ++f0;
+        }
+        const uint32_t off = a, cms[4] = {0u, 1u, 7u, 255u};
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t it = off | (st << 12) | (cms[c] << 24), last = off + cms[c] * st;
+            const uint32_t xs[8] = {0u, off - 1u, off, off + 1u, off + st, last, last + 1u, 4095u};
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t x = min(xs[k], 4095u);  // x < cs <= 4096
+                if (item_next_bf(it, x) != item_next(it, x)) ++f0;
+                if (c == 0 && k < 2 && item_next_bf(kItemEmpty, x) != kNone) ++f0;
+            }
+        }
     }
     for (uint64_t e = gtid; e < (1ull << 31); e += gsz)
         if (cluster_of(ix, uint32_t(e)) != uint32_t(e) / ix.cs) ++f1;
