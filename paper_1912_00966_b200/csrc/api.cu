@@ -502,7 +502,7 @@ bool pick_cluster(eat_handle *h, uint32_t want, int min_stage) {
 bool pick_gasync(eat_handle *h) {
     const int G = eat::gasync_grid(h->hx.n);
     if (G < 1) return false;
-    if (!h->d_gacnt && cudaMalloc(&h->d_gacnt, size_t(G) * 32u * sizeof(uint32_t)) != cudaSuccess) return false;
+    if (!h->d_gacnt && cudaMalloc(&h->d_gacnt, size_t(G) * eat::kGaCntWordsPerCta * sizeof(uint32_t)) != cudaSuccess) return false;
     return true;
 }
 

@@ -92,16 +92,6 @@ __device__ __forceinline__ void cl_or(uint32_t a, uint32_t v) {
     asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(a), "r"(v));
 }
 
-__device__ __forceinline__ uint32_t cl_add(uint32_t a, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
-    return old;
-}
-
-__device__ __forceinline__ void cl_redadd(uint32_t a, uint32_t v) {
-    asm volatile("red.shared::cluster.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-
 __device__ __forceinline__ uint32_t cl_or_old(uint32_t a, uint32_t v) {
     uint32_t old;
     asm volatile("atom.shared::cluster.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
@@ -134,13 +124,17 @@ __device__ __forceinline__ uint32_t lds_volatile(const uint32_t *p) { return *re
 //     hour-cluster record.
 // Staged once per launch (every query of the launch reuses it).
 // ASYNC: no per-sweep cluster barrier at all.  Every CTA loops on its own
-// (take all its marked vertices -> relax them) and the query ends when a
-// counter of marked-or-in-processing vertices in CTA 0 reaches zero: a
-// marking warp adds its marks to the counter (and waits for the add) BEFORE
-// setting the bits, subtracts the marks that hit an already-set bit after,
-// and a CTA subtracts the vertices it took once their relaxations (and the
-// marks they made) are done -- so the counter is >= the pending work at
-// every instant and 0 only at the fixpoint.  Window: all active vertices.
+// (take all its marked vertices -> relax them); per CTA, S counts marks and
+// R finished vertices (local shared memory): a marking warp adds its tries
+// to S (and waits for the add) BEFORE setting the bits, subtracts the tries
+// that lowered nothing and the marks that hit an already-set bit after, and
+// R grows by the vertices a CTA took once their relaxations (and the marks
+// they made) are done; an idle CTA 0 sums every R, then every S (DSMEM):
+// equal sums mean nothing was marked or in processing in between (the grid
+// kernel's two-wave detector, gasync.cu) -- and a fixpoint is stable.
+// (Until round 2 session 3 one pending counter in CTA 0, +tries / -F: every
+// marking warp's add would wait on that one contended word.)  Window: all
+// active vertices.
 template <int STAGE, bool ASYNC>
 __global__ void __launch_bounds__(kClThreads, 1)
     k_query_cluster(DevIndex ix, const uint32_t *__restrict__ src, const uint32_t *__restrict__ tsv, uint64_t nq,
@@ -167,8 +161,9 @@ __global__ void __launch_bounds__(kClThreads, 1)
     __shared__ uint32_t s_tmin[3];                   // window base, rotating (cluster-wide after the push)
     __shared__ uint32_t s_pmin[2], s_pmore[2];       // this CTA's partials of the sweep (parity)
     __shared__ uint32_t s_q[2];                      // query index (lo, hi) pushed by rank 0
-    __shared__ uint32_t s_pend;                      // ASYNC (CTA 0's copy is the one used): pending vertices
-    __shared__ uint32_t s_idle;                      // ASYNC: the counter read 0
+    __shared__ uint32_t s_S, s_R;                    // ASYNC: marks this CTA counted / vertices it finished
+    __shared__ uint32_t s_done;                      // ASYNC (CTA 0's copy is the one used): fixpoint detected
+    __shared__ uint32_t s_idle;                      // ASYNC: CTA 0 raised s_done
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
     const uint32_t window = ix.window;
     const uint32_t e_sa = uint32_t(__cvta_generic_to_shared(e_loc));
@@ -176,7 +171,8 @@ __global__ void __launch_bounds__(kClThreads, 1)
     const uint32_t more_sa = uint32_t(__cvta_generic_to_shared(s_more));
     const uint32_t tmin_sa = uint32_t(__cvta_generic_to_shared(s_tmin));
     const uint32_t q_sa = uint32_t(__cvta_generic_to_shared(s_q));
-    const uint32_t pend0 = cl_map(uint32_t(__cvta_generic_to_shared(&s_pend)), 0u);
+    const uint32_t S_sa = uint32_t(__cvta_generic_to_shared(&s_S)), R_sa = uint32_t(__cvta_generic_to_shared(&s_R));
+    const uint32_t done0 = cl_map(uint32_t(__cvta_generic_to_shared(&s_done)), 0u);
     // DSMEM address of vertex v's arrival / bitmap word in its owner CTA
     auto e_addr = [&](uint32_t v) {
         const uint32_t w = v >> 5;
@@ -282,7 +278,9 @@ __global__ void __launch_bounds__(kClThreads, 1)
             s_tmin[1] = s_tmin[2] = kInf;
             s_pmin[0] = s_pmin[1] = kInf;
             s_pmore[0] = s_pmore[1] = 0;
-            s_pend = rank == 0 ? 1u : 0u;  // ASYNC: the source is marked
+            s_S = rank == 0 ? 1u : 0u;  // ASYNC: the source's mark (counted in CTA 0)
+            s_R = 0;
+            s_done = 0;
         }
         __syncthreads();
         if (tid == 0) {
@@ -328,8 +326,17 @@ __global__ void __launch_bounds__(kClThreads, 1)
 #endif
                 ++sweeps;
                 if (F == 0) {  // idle: is any vertex pending anywhere?
+                    if (rank == 0 && wid == 0) {
+                        // every CTA's R, then (the addresses depend on the sum: issued
+                        // after it returned) every CTA's S; equal -> fixpoint
+                        const uint32_t ra = __reduce_add_sync(0xFFFFFFFFu, lane < ncta ? cl_ld(cl_map(R_sa, lane)) : 0u);
+                        const uint32_t sb = __reduce_add_sync(
+                            0xFFFFFFFFu, lane < ncta ? cl_ld(cl_map(S_sa + (ra & ix.zero), lane)) : 0u);
+                        if (lane == 0 && ra == sb) s_done = 1u;
+                        __syncwarp();
+                    }
                     if (tid == 0) {
-                        s_idle = cl_ld(pend0) == 0u;
+                        s_idle = cl_ld(done0) != 0u;
                         if (!s_idle) __nanosleep(64);
                     }
                     __syncthreads();
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
                         const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
                         const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
                         const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
-                        uint32_t mv = kNone;  // vertex this lane lowered (to be marked)
+                        uint32_t ea = 0, cand = kNone, tv = 0;  // a try: lower e[tv] (at ea) to cand
                         if (qp < tot) {
                             const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
                             const uint32_t eu = lds_volatile(e_loc + ((((u >> 5) >> lg) << 5) | (u & 31u)));
@@ -392,37 +399,46 @@ __global__ void __launch_bounds__(kClThreads, 1)
                                 uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = r0;
                                 const uint32_t kc = cluster_of(ix, eu);
                                 if (eu > tr.first) ldg_crec(ix, cb + kc, r0, r1);
-                                const uint32_t ea = e_addr(tr.v);
+                                ea = e_addr(tr.v);
                                 const uint32_t av = cl_ld(ea);
                                 if (max(eu, tr.first) + tr.lam < av) {
                                     const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan<true>(ix, r0, r1, kc, eu);
-                                    const uint32_t cand = tc + tr.lam;
-                                    if (cand < av && cand < cl_min(ea, cand)) mv = tr.v;
+                                    if (tc + tr.lam < av) {
+                                        cand = tc + tr.lam;
+                                        tv = tr.v;
+                                    }
                                 }
                             }
                         }
                         // (relaxing the lowered vertices at once -- continuation, as in
                         // gasync.cu -- is 11 % slower here: r02_ab_cluster_continuation.jsonl)
-                        const uint32_t wm = __ballot_sync(0xFFFFFFFFu, mv != kNone);
-                        // count the marks in CTA 0 before setting them
-                        if (wm) {
-                            if (lane == uint32_t(__ffs(wm) - 1)) {
-                                // returns once performed in CTA 0: every mark below is
-                                // counted before it can be seen (and un-counted) by its owner
-                                // (per-CTA counters read by a two-wave detector in CTA 0
-                                // instead: same speed, profiles/r02_ab_cluster_termination.jsonl)
-                                cl_add(pend0, uint32_t(__popc(wm)));
-                            }
-                            __syncwarp();
+                        // Lower and mark.  Every lane that tries is counted in CTA 0's
+                        // pending counter by a returning add issued with the atomicMins
+                        // (one round trip for both) and waited for -- the bit address
+                        // depends on its value -- before any bit is set: a mark is
+                        // counted before its owner can see (and un-count) it.  Tries
+                        // that lowered nothing and marks that hit a set bit are
+                        // subtracted after (the counter only over-counts).  (Per-CTA
+                        // counters read by a two-wave detector in CTA 0 instead: same
+                        // speed, profiles/r02_ab_cluster_termination.jsonl)
+                        const uint32_t tm = __ballot_sync(0xFFFFFFFFu, cand != kNone);
+                        if (tm) {
+                            const uint32_t ld = __ffs(tm) - 1u;
+                            uint32_t o = 0;
+                            if (lane == ld) o = atomicAdd(&s_S, uint32_t(__popc(tm)));  // local, returning
+                            const bool low = cand != kNone && cand < cl_min(ea, cand);
+                            o = __shfl_sync(0xFFFFFFFFu, o, ld);
+                            const uint32_t wm = __ballot_sync(0xFFFFFFFFu, low);
                             uint32_t dup = 0;
-                            if (mv != kNone) dup = cl_or_old(bm_addr(mv), 1u << (mv & 31u)) & (1u << (mv & 31u));
+                            if (low) dup = cl_or_old(bm_addr(tv) + (o & ix.zero), 1u << (tv & 31u)) & (1u << (tv & 31u));
                             const uint32_t dm = __ballot_sync(0xFFFFFFFFu, dup != 0u);
-                            if (dm && lane == uint32_t(__ffs(dm) - 1)) cl_redadd(pend0, 0u - uint32_t(__popc(dm)));
+                            const uint32_t extra = uint32_t(__popc(tm)) - uint32_t(__popc(wm)) + uint32_t(__popc(dm));
+                            if (extra && lane == ld) atomicSub(&s_S, extra);
                         }
                     }
                 }
                 __syncthreads();  // every relaxation (and mark count) of the F taken vertices is done
-                if (tid == 0) cl_redadd(pend0, 0u - F);
+                if (tid == 0) atomicAdd(&s_R, F);
 #ifdef EAT_CL_TRACE
                 if (tid == 0 && rank == 0 && sweeps - 1 < 1024) g_cltrace[(sweeps - 1) * 6 + 3] = gtimer();
 #endif

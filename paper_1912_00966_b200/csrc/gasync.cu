@@ -14,9 +14,11 @@
 // all active vertices are taken (the paper's topology-driven schedule, any
 // order reaches the same fixpoint).
 // Termination (no barrier to count "nothing changed" at): per CTA, S counts
-// the marks it set (incremented with a returning atomic BEFORE the bits are
-// set, decremented for marks that hit an already-set bit) and R the vertices
-// whose relaxations it finished.  When CTA 0 is idle it sums every R, then
+// the marks it set (a warp adds every lane that tries to lower an e[v] with
+// a returning atomic issued beside the atomicMins and waited for BEFORE the
+// bits are set -- the bit address depends on its value; the tries that
+// lowered nothing and the marks that hit an already-set bit are subtracted
+// after) and R the vertices whose relaxations it finished.  When CTA 0 is idle it sums every R, then
 // every S; both are monotone in the true counts and a mark is counted in S
 // before its bit is visible, so sum(R) read first == sum(S) read second means
 // nothing was marked or in processing at any instant between the two reads
@@ -32,7 +34,13 @@ namespace {
 
 using namespace dev;
 
-constexpr uint32_t kGaCntStride = 32;  // S, R of CTA c at cnt[c * 32 + 0 / 1] (own 128-byte line)
+// Counters of CTA c at cnt[c * kGaCntCta ...]: S of warp k at + 8 k (one
+// 32-byte sector each: a warp's returning S add meets no other warp's), R at
+// + kGaRWord.  Per-warp S: the add a marking warp waits for is uncontended
+// (one counter per CTA: single queries 7-8 % slower, r02_ab_spec_count.jsonl).
+constexpr uint32_t kGaRWord = 32u * 8u;
+constexpr uint32_t kGaCntCta = kGaRWord + 8u;
+static_assert(kGaCntCta <= kGaCntWordsPerCta, "counter block");
 
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) { return __ldcv(p); }  // fetched again (L2)
 
@@ -69,11 +77,12 @@ __global__ void __launch_bounds__(kGaThreads, 1)
     uint32_t *list = reinterpret_cast<uint32_t *>(rng + Wl * 32u);  // [32 Wl] taken vertices
     __shared__ uint32_t s_cnt[2];
     __shared__ uint32_t s_done;
+    __shared__ uint32_t s_red[2];  // CTA 0's detector: sum of R, sum of S
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
     const uint64_t gtid = uint64_t(c) * kGaThreads + tid, gsz = uint64_t(G) * kGaThreads;
     uint32_t *bar = w.ctl + kBarWord;  // monotonic grid-barrier counter (zeroed per launch)
     uint32_t bar_epoch = 0;
-    uint32_t *myS = w.cnt + c * kGaCntStride, *myR = myS + 1;
+    uint32_t *myS = w.cnt + c * kGaCntCta + wid * 8u, *myR = w.cnt + c * kGaCntCta + kGaRWord;
 
     // ---- stage the owned vertices' index; initialize (Alg. 2)
     for (uint32_t li = tid; li < Wl * 32u; li += kGaThreads) {
@@ -87,8 +96,8 @@ __global__ void __launch_bounds__(kGaThreads, 1)
     }
     for (uint64_t i = gtid; i < n; i += gsz) w.arr[i] = kInf;
     for (uint64_t i = gtid; i < W; i += gsz) w.bm[i] = 0;
+    if (lane == 0) myS[0] = 0;
     if (tid == 0) {
-        myS[0] = 0;
         myR[0] = 0;
         s_cnt[0] = s_cnt[1] = 0;
         s_done = 0;
@@ -99,15 +108,17 @@ __global__ void __launch_bounds__(kGaThreads, 1)
         const uint32_t si = __ldg(ix.perm + s);
         w.arr[si] = ts;
         w.bm[si >> 5] = 1u << (si & 31u);
-        atomicAdd(w.cnt + ((si >> 5) % G) * kGaCntStride, 1u);  // the source's mark, counted by its owner
+        atomicAdd(w.cnt + ((si >> 5) % G) * kGaCntCta, 1u);  // the source's mark, counted by its owner (warp 0's S)
     }
     grid_sync(bar, bar_epoch, G);
 
-    // relax type t of a source with arrival eu; returns the target it lowered
-    auto relax = [&](uint32_t eu, uint32_t t) -> uint32_t {
+    // candidate arrival at v = tr.v through type t of a source with arrival
+    // eu (Alg. 3 up to the atomicMin); kNone if it cannot lower e[v]
+    auto prep = [&](uint32_t eu, uint32_t t, uint32_t &v) -> uint32_t {
         const uint32_t cb = __ldg(ix.type_cb + t);
         TypeRec tr = load_type(ix, t);
         tr.last |= cb & ix.zero;
+        v = tr.v;
         if (eu > tr.last) return kNone;
         uint4 r0 = make_uint4(0u, 0u, 0u, 0u), r1 = r0;
         const uint32_t kc = cluster_of(ix, eu);
@@ -116,18 +127,49 @@ __global__ void __launch_bounds__(kGaThreads, 1)
         if (max(eu, tr.first) + tr.lam >= av) return kNone;
         const uint32_t tc = eu <= tr.first ? tr.first : cluster_scan<true>(ix, r0, r1, kc, eu);
         const uint32_t cand = tc + tr.lam;
-        return (cand < av && cand < atomicMin(w.arr + tr.v, cand)) ? tr.v : kNone;
+        return cand < av ? cand : kNone;
+    };
+    // relax type t of a source with arrival eu; returns the target it lowered
+    auto relax = [&](uint32_t eu, uint32_t t) -> uint32_t {
+        uint32_t v;
+        const uint32_t cand = prep(eu, t, v);
+        return (cand != kNone && cand < atomicMin(w.arr + v, cand)) ? v : kNone;
+    };
+    // set bit v of the marked bitmap; 1 if it was already set.  `o` is the
+    // value a returning S add gave this warp: the address depends on it, so
+    // the bit is set only after that add is performed (counted before seen)
+    auto set_mark = [&](uint32_t v, uint32_t o) -> uint32_t {
+        const uint32_t bit = 1u << (v & 31u);
+        return (atomicOr(w.bm + (v >> 5) + (o & ix.zero), bit) & bit) != 0u;
     };
     // mark the lanes' lowered vertices (wm: ballot of mv != kNone; warp-uniform)
     auto mark = [&](uint32_t mv, uint32_t wm) {
         if (!wm) return;
-        // counted in S (returning atomic: performed) before any bit is set
-        if (lane == uint32_t(__ffs(wm) - 1)) atomicAdd(myS, uint32_t(__popc(wm)));
-        __syncwarp();
-        uint32_t dup = 0;
-        if (mv != kNone) dup = atomicOr(w.bm + (mv >> 5), 1u << (mv & 31u)) & (1u << (mv & 31u));
-        const uint32_t dm = __ballot_sync(0xFFFFFFFFu, dup != 0u);
-        if (dm && lane == uint32_t(__ffs(dm) - 1)) atomicSub(myS, uint32_t(__popc(dm)));
+        const uint32_t ld = __ffs(wm) - 1u;
+        uint32_t o = 0;
+        if (lane == ld) o = atomicAdd(myS, uint32_t(__popc(wm)));  // counted in S first
+        o = __shfl_sync(0xFFFFFFFFu, o, ld);
+        const uint32_t dm = __ballot_sync(0xFFFFFFFFu, mv != kNone && set_mark(mv, o));
+        if (dm && lane == ld) atomicSub(myS, uint32_t(__popc(dm)));
+    };
+    // lower e[v] to cand (lanes with cand != kNone) and mark the v lowered:
+    // the S add is issued with the atomicMins, speculatively for every lane
+    // that tries (one round trip for both), and waited for before any bit is
+    // set; tries that did not lower e[v] and marks that hit a set bit are
+    // subtracted afterwards (S only ever over-counts: termination is delayed,
+    // never early)
+    auto lower_mark = [&](uint32_t v, uint32_t cand) {
+        const uint32_t tm = __ballot_sync(0xFFFFFFFFu, cand != kNone);
+        if (!tm) return;
+        const uint32_t ld = __ffs(tm) - 1u;
+        uint32_t o = 0;
+        if (lane == ld) o = atomicAdd(myS, uint32_t(__popc(tm)));
+        const bool low = cand != kNone && cand < atomicMin(w.arr + v, cand);
+        o = __shfl_sync(0xFFFFFFFFu, o, ld);
+        const uint32_t wm = __ballot_sync(0xFFFFFFFFu, low);
+        const uint32_t dm = __ballot_sync(0xFFFFFFFFu, low && set_mark(v, o));
+        const uint32_t extra = uint32_t(__popc(tm)) - uint32_t(__popc(wm)) + uint32_t(__popc(dm));
+        if (extra && lane == ld) atomicSub(myS, extra);
     };
 
     uint32_t iters = 0;
@@ -152,19 +194,25 @@ __global__ void __launch_bounds__(kGaThreads, 1)
         const uint32_t F = s_cnt[p];
         if (tid == 0) s_cnt[p ^ 1u] = 0;
         if (F == 0) {  // idle: termination detection (CTA 0) / poll
-            if (wid == 0) {
-                if (c == 0) {
-                    uint32_t ra = 0, sb = 0;
-                    for (uint32_t x = lane; x < G; x += 32u) ra += ld_volatile(w.cnt + x * kGaCntStride + 1);
-                    ra = __reduce_add_sync(0xFFFFFFFFu, ra);
-                    for (uint32_t x = lane; x < G; x += 32u) sb += ld_volatile(w.cnt + x * kGaCntStride);
-                    sb = __reduce_add_sync(0xFFFFFFFFu, sb);
-                    if (lane == 0 && ra == sb) __stcg(w.ctl, 1u);
-                }
-                if (lane == 0) {
-                    s_done = ld_volatile(w.ctl);
-                    if (!s_done) __nanosleep(100);
-                }
+            if (c == 0) {  // every R, then every S (all of CTA 0's threads read)
+                if (tid == 0) s_red[0] = s_red[1] = 0u;
+                __syncthreads();
+                uint32_t ra = 0;
+                for (uint32_t x = tid; x < G; x += kGaThreads) ra += ld_volatile(w.cnt + x * kGaCntCta + kGaRWord);
+                ra = __reduce_add_sync(0xFFFFFFFFu, ra);
+                if (lane == 0 && ra) atomicAdd(&s_red[0], ra);
+                __syncthreads();  // every R read returned before any S read is issued
+                uint32_t sb = 0;
+                for (uint32_t x = tid; x < 32u * G; x += kGaThreads)
+                    sb += ld_volatile(w.cnt + (x >> 5) * kGaCntCta + (x & 31u) * 8u);
+                sb = __reduce_add_sync(0xFFFFFFFFu, sb);
+                if (lane == 0 && sb) atomicAdd(&s_red[1], sb);
+                __syncthreads();
+                if (tid == 0 && s_red[0] == s_red[1]) __stcg(w.ctl, 1u);
+            }
+            if (tid == 0) {
+                s_done = ld_volatile(w.ctl);
+                if (!s_done) __nanosleep(100);
             }
             __syncthreads();
             if (s_done || iters > (1u << 22)) break;  // (watchdog: never reached by a correct run)
@@ -232,9 +280,9 @@ __global__ void __launch_bounds__(kGaThreads, 1)
                         const uint32_t c_nt = __shfl_sync(0xFFFFFFFFu, cnt, L2);
                         const uint32_t c_p0 = __shfl_sync(0xFFFFFFFFu, cp0, L2);
                         const uint32_t cu = __shfl_sync(0xFFFFFFFFu, cx, L2);
-                        uint32_t mv2 = kNone;
-                        if (cq < ctot) mv2 = relax(__ldcg(w.arr + cu), c_p0 + (cq - (c_incl - c_nt)));
-                        mark(mv2, __ballot_sync(0xFFFFFFFFu, mv2 != kNone));
+                        uint32_t v2 = 0, cand2 = kNone;
+                        if (cq < ctot) cand2 = prep(__ldcg(w.arr + cu), c_p0 + (cq - (c_incl - c_nt)), v2);
+                        lower_mark(v2, cand2);
                     }
                     wm = 0;
                 }

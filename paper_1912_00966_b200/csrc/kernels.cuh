@@ -147,10 +147,11 @@ cudaError_t launch_query_cluster(const DevIndex &ix, const ClusterArgs &a, cudaS
 int cluster_max_active(uint32_t n, int cs, int stage, uint32_t tl_cap, bool async);
 
 // Scratch of the barrier-free grid kernel (gasync.cu, EAT_KERNEL_GRID_ASYNC).
+constexpr uint32_t kGaCntWordsPerCta = 288;  // gasync.cu: 32 per-warp S sectors + R
 struct GAsyncWork {
     uint32_t *arr;   // [n] arrival times, internal ids
     uint32_t *bm;    // [W] marked-vertex bitmap
-    uint32_t *cnt;   // [32 * grid] per-CTA counters: S (marks set), R (vertices done)
+    uint32_t *cnt;   // [kGaCntWordsPerCta * grid] per-CTA counters: S per warp (marks set), R (vertices done)
     uint32_t *ctl;   // [kCtlWords]: 0 done flag, 8 iterations of CTA 0, kBarWord grid barrier
 };
 // CTAs of the launch for n vertices (one per SM; 0 if the per-CTA slices do not fit shared memory).

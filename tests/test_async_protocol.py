@@ -1,13 +1,18 @@
 """CPU models of the termination protocols of the asynchronous kernels
 (no barrier between relaxations):
 
-* grid-async (csrc/gasync.cu): per-CTA counters S (marks set, counted
-  BEFORE the bit is set, minus marks that hit an already-set bit) and R
-  (taken vertices whose relaxations finished); an idle CTA 0 sums every R,
-  then every S, and stops everyone when the sums are equal;
-* cluster-async (csrc/cluster.cu ASYNC): one pending counter (+k before
-  marking, -dups after, -F after finishing F taken vertices); idle CTAs
-  stop when it reads 0.
+* "grid" -- the two-wave S/R protocol of both asynchronous kernels
+  (csrc/gasync.cu: S per warp, R per CTA, in global memory; csrc/cluster.cu
+  ASYNC: S and R per CTA in shared memory, read through DSMEM): S counts
+  marks (counted BEFORE the bit is set, minus marks that hit an already-set
+  bit), R taken vertices whose relaxations finished; an idle CTA 0 sums
+  every R, then every S, and stops everyone when the sums are equal (the
+  model keeps one S per CTA: finer counters only spread the same sums);
+* "cluster" -- one pending counter (+k before marking, -dups after, -F
+  after finishing F taken vertices; idle CTAs stop when it reads 0): the
+  cluster kernel's protocol until round 2 session 3, kept as a checked
+  alternative (every marking warp waiting on one shared word made the
+  kernel 7 % slower once the wait was enforced).
 
 Every shared-memory access of the protocol is one step of a generator; a
 seeded random scheduler interleaves the "CTAs" one step at a time (the
@@ -16,6 +21,11 @@ stop is decided, no vertex is marked and none is being processed (no false
 termination), and the final arrivals equal the serial CSA oracle.  A
 deliberately broken variant (S counted AFTER the bit is set) must be caught
 by the same check for some interleaving -- the test has teeth.
+Speculative counting (``spec``, the kernels since round 2 session 3): a
+warp counts every lane that TRIES to lower e[v] before its atomicMins (the
+count and the atomicMins share one round trip), sets the bits of the
+vertices it lowered, then subtracts the tries that lowered nothing and the
+marks that hit a set bit.
 
 The relaxation itself is a test-side model on the raw connections (the CUDA
 relaxation is covered by the GPU parity tests); what is tested is the
@@ -55,7 +65,7 @@ class _World:
         return any(self.bits) or any(self.processing)
 
 
-def _cta(wd, me, protocol, broken, log):
+def _cta(wd, me, protocol, broken, log, spec=False):
     """One CTA: a generator, one shared-memory access per step."""
     while True:
         # take every marked vertex this CTA owns (atomicExch per vertex)
@@ -95,7 +105,36 @@ def _cta(wd, me, protocol, broken, log):
             yield
             eu = wd.e[u]
             lowered = []
-            for v, d, l in wd.out[u]:
+            if spec:
+                tries = []
+                for v, d, l in wd.out[u]:
+                    yield
+                    if d >= eu and d + l < wd.e[v]:  # e[v] read: this lane will try
+                        tries.append((v, d + l))
+                if tries:
+                    yield  # the returning count, before any atomicMin or bit
+                    if protocol == "grid":
+                        wd.S[me] += len(tries)
+                    else:
+                        wd.pend += len(tries)
+                    for v, c in tries:
+                        yield
+                        if c < wd.e[v]:  # atomicMin
+                            wd.e[v] = c
+                            lowered.append(v)
+                    dups = 0
+                    for v in lowered:
+                        yield
+                        if wd.bits[v]:
+                            dups += 1
+                        wd.bits[v] = True
+                    yield  # un-count the tries that lowered nothing and the duplicates
+                    if protocol == "grid":
+                        wd.S[me] -= len(tries) - len(lowered) + dups
+                    else:
+                        wd.pend -= len(tries) - len(lowered) + dups
+                lowered = []
+            for v, d, l in ([] if spec else wd.out[u]):
                 if d >= eu and d + l < wd.e[v]:
                     yield
                     if d + l < wd.e[v]:  # atomicMin
@@ -138,10 +177,10 @@ def _cta(wd, me, protocol, broken, log):
         wd.processing[me] = 0
 
 
-def _run(tt, s, t_s, P, protocol, broken, seed, max_steps=2_000_000):
+def _run(tt, s, t_s, P, protocol, broken, seed, max_steps=2_000_000, spec=False):
     wd = _World(tt, s, t_s, P)
     log = []
-    ctas = [_cta(wd, me, protocol, broken, log) for me in range(P)]
+    ctas = [_cta(wd, me, protocol, broken, log, spec) for me in range(P)]
     live = list(range(P))
     rng = random.Random(seed)
     steps = 0
@@ -170,10 +209,12 @@ def test_async_termination_protocols_match_oracle():
         want = oracle.CSA(tt.num_vertices, *tt.arrays()).query(s, t_s)
         for protocol in ("grid", "cluster"):
             for P in (1, 2, 3, 5):
-                wd, log = _run(tt, s, t_s, P, protocol, broken=False, seed=seed * 31 + P)
-                assert log and not any(log), f"{protocol} P={P} seed={seed}: stop decided with work pending"
-                assert not wd.pending_work()
-                assert np.array_equal(np.array(wd.e, dtype=np.uint32), want), f"{protocol} P={P} seed={seed}"
+                for spec in (False, True):
+                    wd, log = _run(tt, s, t_s, P, protocol, broken=False, seed=seed * 31 + P, spec=spec)
+                    tag = f"{protocol} P={P} spec={spec} seed={seed}"
+                    assert log and not any(log), f"{tag}: stop decided with work pending"
+                    assert not wd.pending_work()
+                    assert np.array_equal(np.array(wd.e, dtype=np.uint32), want), tag
 
 
 def test_counting_after_marking_is_caught():
