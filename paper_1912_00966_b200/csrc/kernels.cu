@@ -274,10 +274,13 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
         unsigned long long c_sel_loop = 0, c_pair_loop = 0;  // slowest warp's own loop time
         if (COUNT && tid == 0) s_tw[0] = s_tw[1] = 0;
         // rotating s_tmin slots: t_cur = sweep % 3 (this sweep's window base),
-        // t_nxt = (sweep + 1) % 3 (written by this sweep), t_old = (sweep + 2) % 3
-        uint32_t t_cur = 0, t_nxt = 1, t_old = 2;
+        // t_nxt = (sweep + 1) % 3 (written by this sweep), t_old = (sweep + 2) % 3;
+        // only t_cur is carried across sweeps (registers are the kernel's
+        // limit: 32 at five 384-thread CTAs per SM)
+        uint32_t t_cur = 0;
         for (;;) {
             const uint32_t p = sweeps & 1u;
+            const uint32_t t_nxt = t_cur == 2u ? 0u : t_cur + 1u, t_old = t_cur == 0u ? 2u : t_cur - 1u;
             uint32_t thr = kInf;
             if (window < kInf) {
                 const uint32_t base = s_tmin[t_cur];
@@ -373,6 +376,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                     if (lane >= uint32_t(o)) incl += y;
                 }
                 const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                const uint32_t pbase = p0 - (incl - nt);
                 // (measured alternatives, profiles/r02_ab_owner_search_variants.jsonl:
                 // a start-bitmask + shared-memory owner map -1 %, e[u] read once per
                 // chunk and shuffled -2 %: the per-pair read sees fresher arrivals;
@@ -387,12 +391,11 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                         const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, L + step - 1u);
                         if (v <= qp) L += step;
                     }
-                    const uint32_t o_incl = __shfl_sync(0xFFFFFFFFu, incl, L);
-                    const uint32_t o_nt = __shfl_sync(0xFFFFFFFFu, nt, L);
-                    const uint32_t o_p0 = __shfl_sync(0xFFFFFFFFu, p0, L);
+                    // type of pair qp = p0 - (incl - nt) + qp of its owner: one shuffle
+                    const uint32_t t = __shfl_sync(0xFFFFFFFFu, pbase, L) + qp;
                     const uint32_t u = __shfl_sync(0xFFFFFFFFu, x, L);
                     if (qp >= tot) continue;
-                    const uint32_t t = o_p0 + (qp - (o_incl - o_nt));
+                    const uint32_t o_p0 = COUNT ? __ldg(ix.type_ptr + u) : t;  // first type of u (COUNT)
                     const uint32_t eu = ar.get(u);
                     // the cluster base goes out with the header (a lazy load after
                     // the early-termination tests costs -5 %: one more dependent hop,
@@ -455,60 +458,59 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
                 s_tw[1] = 0;
             }
             ++sweeps;
-            {
-                const uint32_t tmp = t_cur;
-                t_cur = t_nxt;
-                t_nxt = t_old;
-                t_old = tmp;
-            }
+            t_cur = t_nxt;
             if (s_more[p] == 0u) break;  // nothing deferred, nothing lowered: fixpoint
             if (A16 && s_ovf) break;      // recomputed by the uint32 variant
         }
-        if (A16 && s_ovf) {
-            if (tid == 0) ovf_list[atomicAdd(ovf_cnt, 1u)] = uint32_t(q);
-            __syncthreads();
-            continue;
-        }
-        // Output in caller ids
-        if (TGT) {
-            if (tid == 0) orow[0] = ar.get(di);
-        } else if ((n & 3u) == 0u && (reinterpret_cast<uintptr_t>(orow) & 15u) == 0u) {
-            // 16-byte stores (rows may live in mapped host memory: eat_query_many direct mode)
-            const uint4 *pv = reinterpret_cast<const uint4 *>(ix.perm);
-            uint4 *ov = reinterpret_cast<uint4 *>(orow);
-            for (uint32_t i = tid; i < n / 4u; i += kCtaThreads) {
-                const uint4 pi = __ldg(pv + i);
-                ov[i] = make_uint4(ar.get(pi.x), ar.get(pi.y), ar.get(pi.z), ar.get(pi.w));
+        {  // q and the row pointer re-derived from shared memory: not live across the sweeps
+            const unsigned long long q = *reinterpret_cast<volatile unsigned long long *>(&s_q);
+            uint32_t *orow = TGT ? out + q : out + q * uint64_t(n);
+            if (A16 && s_ovf) {
+                if (tid == 0) ovf_list[atomicAdd(ovf_cnt, 1u)] = uint32_t(q);
+                __syncthreads();
+                continue;
             }
-        } else {
-            for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = ar.get(__ldg(ix.perm + i));
-        }
-        if (tid == 0 && sweeps_out) sweeps_out[q] = sweeps;
-        if (COUNT) {
-            unsigned long long v[10] = {c_vis, c_type, c_crec, c_spill, c_impr, c_edge, c_runs, c_singles, c_fb,
-                                        c_selbits};
-            const int slot[10] = {0, 1, 2, 3, 4, 10, 11, 12, 13, 14};
-            for (int k = 0; k < 10; ++k) {
-                for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o);
-                if (lane == 0 && v[k]) atomicAdd(counters + slot[k], v[k]);
+            // Output in caller ids
+            if (TGT) {
+                if (tid == 0) orow[0] = ar.get(di);
+            } else if ((n & 3u) == 0u && (reinterpret_cast<uintptr_t>(orow) & 15u) == 0u) {
+                // 16-byte stores (rows may live in mapped host memory: eat_query_many direct mode)
+                const uint4 *pv = reinterpret_cast<const uint4 *>(ix.perm);
+                uint4 *ov = reinterpret_cast<uint4 *>(orow);
+                for (uint32_t i = tid; i < n / 4u; i += kCtaThreads) {
+                    const uint4 pi = __ldg(pv + i);
+                    ov[i] = make_uint4(ar.get(pi.x), ar.get(pi.y), ar.get(pi.z), ar.get(pi.w));
+                }
+            } else {
+                for (uint32_t i = tid; i < n; i += kCtaThreads) orow[i] = ar.get(__ldg(ix.perm + i));
             }
-            if (tid == 0) {
-                atomicAdd(counters + 5, (unsigned long long)sweeps);
-                atomicAdd(counters + 6, c_sel_cyc);
-                atomicAdd(counters + 7, c_pair_cyc);
-                atomicAdd(counters + 8, c_sel_loop);
-                atomicAdd(counters + 9, c_pair_loop);
+            if (tid == 0 && sweeps_out) sweeps_out[q] = sweeps;
+            if (COUNT) {
+                unsigned long long v[10] = {c_vis, c_type, c_crec, c_spill, c_impr, c_edge, c_runs, c_singles, c_fb,
+                                            c_selbits};
+                const int slot[10] = {0, 1, 2, 3, 4, 10, 11, 12, 13, 14};
+                for (int k = 0; k < 10; ++k) {
+                    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o);
+                    if (lane == 0 && v[k]) atomicAdd(counters + slot[k], v[k]);
+                }
+                if (tid == 0) {
+                    atomicAdd(counters + 5, (unsigned long long)sweeps);
+                    atomicAdd(counters + 6, c_sel_cyc);
+                    atomicAdd(counters + 7, c_pair_cyc);
+                    atomicAdd(counters + 8, c_sel_loop);
+                    atomicAdd(counters + 9, c_pair_loop);
+                }
             }
-        }
-        if (done) {
-            // streamed e2e (eat_query_many, page-locked output): flag the
-            // finished row in mapped host memory once every thread's row
-            // stores are visible system-wide (one plain store per query: no
-            // atomics on host memory, which PCIe hosts need not support); the
-            // host copies a chunk as soon as all its rows are flagged
-            __threadfence_system();
-            __syncthreads();
-            if (tid == 0) *reinterpret_cast<volatile unsigned int *>(done + q) = 1u;
+            if (done) {
+                // streamed e2e (eat_query_many, page-locked output): flag the
+                // finished row in mapped host memory once every thread's row
+                // stores are visible system-wide (one plain store per query: no
+                // atomics on host memory, which PCIe hosts need not support); the
+                // host copies a chunk as soon as all its rows are flagged
+                __threadfence_system();
+                __syncthreads();
+                if (tid == 0) *reinterpret_cast<volatile unsigned int *>(done + q) = 1u;
+            }
         }
         __syncthreads();
     }
