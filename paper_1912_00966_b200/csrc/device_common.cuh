@@ -62,11 +62,14 @@ __device__ __forceinline__ uint32_t cluster_of(const DevIndex &ix, uint32_t e) {
 // given the cluster's 32-byte record (r0, r1): smallest term >= eu among the
 // cluster's APs, else the first departure of the next non-empty cluster
 // (precomputed as next_min).  Precondition: first < eu <= last.
-// LAT (latency-bound single-query kernels): items 0 and 1 -- most slots hold
-// one or two -- are evaluated without branches and the rest only if item 1
-// starts before x (city / metro single query -2 % / -3 %); the throughput-
-// bound batched kernel keeps the early exits (its instruction count decides:
-// -0.5 % with LAT, profiles/r02_ab_scan_lat.jsonl).
+// Item 0 (most slots hold one AP run) is evaluated without branches and the
+// rest only if item 1 exists and item 0 starts before x (batched kernel
+// +1.5 %, profiles/r02_ab_scan_first_item.jsonl).  LAT (latency-bound
+// single-query kernels): items 0 and 1 without branches, the rest only if
+// item 1 starts before x (city / metro / country single query -2.2 / -2.8 /
+// -2.5 % against the loop with early exits, 1-2 % faster than one
+// branch-free item there; in the batched kernel -0.5 %:
+// profiles/r02_ab_scan_lat.jsonl).
 template <bool LAT = false>
 __device__ __forceinline__ uint32_t cluster_scan(const DevIndex &ix, const uint4 &r0, const uint4 &r1, uint32_t k,
                                                  uint32_t eu) {
@@ -90,12 +93,15 @@ __device__ __forceinline__ uint32_t cluster_scan(const DevIndex &ix, const uint4
             }
         }
     } else {
-        const uint32_t items[kInlineItems] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        best = item_next_bf(r0.y, x);
+        if (r0.z != kItemEmpty && (r0.y & 0xFFFu) < x) {
+            const uint32_t items[kInlineItems - 1] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
-        for (int i = 0; i < kInlineItems; ++i) {
-            if (items[i] == kItemEmpty) break;  // slots are filled from the front
-            best = min(best, item_next(items[i], x));
-            if ((items[i] & 0xFFFu) >= x) break;
+            for (int i = 0; i < kInlineItems - 1; ++i) {
+                if (items[i] == kItemEmpty) break;  // slots are filled from the front
+                best = min(best, item_next(items[i], x));
+                if ((items[i] & 0xFFFu) >= x) break;
+            }
         }
     }
     return best != kNone ? k * ix.cs + best : r0.x;
