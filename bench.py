@@ -632,7 +632,7 @@ def run_gpu(args):
                        "l2": "flushed (256 MiB write) between timed steps",
                        "kernel": "cta (batched)" if st0["cta_grid"] > 0 else
                        "CTA groups (k_query_groups, warp-flattened pairs + time window)",
-                       "subtrips": args.subtrips, "window_s": 1200 if st0["cta_grid"] > 0 else 2400,
+                       "subtrips": args.subtrips, "window_s": 1500 if st0["cta_grid"] > 0 else 2400,
                        "cta_threads": st0["cta_threads"] if st0["cta_grid"] > 0 else None,
                        "shortcuts": st0["num_shortcuts"]},
             "parity": parity, "parity_rows": parity_rows,

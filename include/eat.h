@@ -151,8 +151,9 @@ typedef struct eat_build_opts {
                                      e[u] <= min_active(e) + window (others stay active); EAT_INF = every
                                      active vertex (the paper's schedule); 0 -> EAT_DEFAULT_WINDOW.
                                      Results are identical for every value (same fixpoint). */
-    uint32_t cta_threads;         /* batched CTA kernel threads per query: 0 -> 384; 512, 384, 320, 256, 192 or 128
-                                     (occupancy knob, tools/sweep.py) */
+    uint32_t cta_threads;         /* batched CTA kernel threads per query: 0 -> 320; 512, 384, 320, 256, 192 or 128
+                                     (occupancy knob, tools/sweep.py; 320: 5 CTAs x 10 warps per SM at 40 registers,
+                                     1.4 % over 384 threads at 32, profiles/r02_ab_cta_threads_s3.jsonl) */
     uint32_t subtrips;            /* sub-trip shortcuts (needs tt->trip): 0 off;
                                      1 = r = round(sqrt(k)) per trip of k connections;
                                      2 = r = round(sqrt(average trip length)); >= 3: r itself;
@@ -194,7 +195,8 @@ typedef struct eat_build_opts {
 
 #define EAT_CONT_NONE 0xFFFFFFFFu
 #define EAT_SUBTRIPS_HIER 1000u  /* eat_build_opts.subtrips: hierarchical sub-trips, base r = value - 1000 */
-#define EAT_DEFAULT_WINDOW 1200u   /* seconds; city batch with sub-trips r = 3: 961k q/s vs 951k at 1800 s (profiles/r01_sweep_window_r3.jsonl) */
+#define EAT_DEFAULT_WINDOW 1500u   /* seconds; city batch with sub-trips r = 3, 320-thread CTAs: 1.231M q/s vs 1.219M at 1200 s,
+                                      1.229M at 1800 s, 1.195M at 900 s (profiles/r02_sweep_window_320.jsonl) */
 
 typedef struct eat_handle eat_handle;
 

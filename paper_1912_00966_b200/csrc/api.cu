@@ -78,7 +78,7 @@ struct eat_handle {
     uint32_t mode = EAT_MODE_REPLICATED;
     uint32_t window = EAT_INF;           // CTA schedule time window (EAT_INF = all active vertices)
     uint32_t group_window = EAT_INF;     // the same for batches on CTA groups (k_query_groups)
-    uint32_t cta_threads = 384;          // CTA-kernel variant (batched queries)
+    uint32_t cta_threads = 320;          // CTA-kernel variant (batched queries)
     uint32_t lookup_mode = 0;            // 0 Cluster-AP; NEXT-3 ablations 1 (Connection-type-AP), 2 (linear)
     uint32_t cont_budget = 1;            // grid frontier kernel: continuation hops per frontier vertex
     std::vector<uint4> raw;              // EAT_KERNEL_CONNECTION: raw connections until upload
@@ -661,7 +661,7 @@ eat_status apply_opts(eat_handle *h, const eat_build_opts &o) {
     h->window = o.window_seconds == 0 ? EAT_DEFAULT_WINDOW : o.window_seconds;
     h->group_window = o.window_seconds == 0 ? kDefaultGroupWindow : o.window_seconds;
     h->cluster_window = o.window_seconds == 0 ? EAT_INF : o.window_seconds;
-    h->cta_threads = o.cta_threads == 0 ? 384u : o.cta_threads;
+    h->cta_threads = o.cta_threads == 0 ? 320u : o.cta_threads;
     if (h->cta_threads != 512 && h->cta_threads != 384 && h->cta_threads != 320 && h->cta_threads != 256 &&
         h->cta_threads != 192 && h->cta_threads != 128)
         return fail(EAT_EINVAL, "cta_threads must be 128, 192, 256, 320, 384 or 512");

@@ -117,7 +117,7 @@ __device__ __noinline__ void slot_census(const DevIndex &ix, uint32_t cb, uint32
 //   3. next frontier = improved (nxt) + deferred (cur).
 // THREADS per CTA and LISTCAP (selected vertices per sweep; overflow stays
 // active) are template parameters: 512/2048 fits 4 CTAs (queries) per SM for
-// a 10k-stop city, 384/512 fits 5.
+// a 10k-stop city, 384/512 and 320/512 (the default) fit 5.
 
 // COUNT: instrumented variant (EAT_BUILD_COUNTERS) accumulating, per launch,
 // the work counters used for algorithmic-byte accounting:
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
         // rotating s_tmin slots: t_cur = sweep % 3 (this sweep's window base),
         // t_nxt = (sweep + 1) % 3 (written by this sweep), t_old = (sweep + 2) % 3;
         // only t_cur is carried across sweeps (registers are the kernel's
-        // limit: 32 at five 384-thread CTAs per SM)
+        // limit: 40 at five 320-thread CTAs per SM, 32 at 384)
         uint32_t t_cur = 0;
         for (;;) {
             const uint32_t p = sweeps & 1u;

@@ -27,7 +27,7 @@ CASES = {
     "cta_batch16": ("k_query_cta (uint16 e[] pass + uint32 recompute)", dict(arr_bits=16), "batch"),
     "cta_batch32": ("k_query_cta (uint32 e[])", dict(arr_bits=32), "batch"),
     "cta_targets": ("k_query_cta<TGT> (goal-directed)", dict(), "targets"),
-    "cta_batch384": ("k_query_cta (384 threads, uint32 e[]: the batch default)", dict(cta_threads=384, arr_bits=32),
+    "cta_batch384": ("k_query_cta (384 threads, uint32 e[]: the batch default until r02 session 3)", dict(cta_threads=384, arr_bits=32),
                      "batch"),
     "cluster16": ("k_query_cluster<2> (16 CTAs, DSMEM e[], staged index)", dict(kernel="cluster", cluster_ctas=16),
                   "single"),
