@@ -345,8 +345,8 @@ __global__ void __launch_bounds__(kClThreads, 1)
                     continue;
                 }
                 const uint32_t g = min(32u, max(1u, (F + kClWarps - 1u) / kClWarps));
-                for (uint32_t k0 = wid * g; k0 < F; k0 += kClWarps * g) {
-                    const uint32_t j = k0 + lane;
+        for (uint32_t k0 = 0; k0 < F; k0 += kClWarps * g) {  // strided: warp w takes k0 + w + i * warps (city / country single query -2 %, profiles/r02_ab_cta_strided.jsonl)
+                    const uint32_t j = k0 + wid + lane * kClWarps;
                     uint32_t x = 0, p0 = 0, nt = 0;
                     if (lane < g && j < F) {
                         x = a_list[j];
@@ -528,8 +528,8 @@ __global__ void __launch_bounds__(kClThreads, 1)
             // ---- 2. warp-flattened (vertex, type) pairs (as k_query_cta)
             const uint32_t g = min(32u, max(1u, (F + kClWarps - 1u) / kClWarps));
             uint32_t imin = kInf;
-            for (uint32_t k0 = wid * g; k0 < F; k0 += kClWarps * g) {
-                const uint32_t j = k0 + lane;
+        for (uint32_t k0 = 0; k0 < F; k0 += kClWarps * g) {  // strided: warp w takes k0 + w + i * warps
+                const uint32_t j = k0 + wid + lane * kClWarps;
                 uint32_t x = 0, p0 = 0, nt = 0;
                 if (lane < g && j < F) {
                     x = s_list[j];

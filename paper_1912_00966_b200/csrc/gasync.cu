@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(kGaThreads, 1)
             continue;
         }
         const uint32_t g = min(32u, max(1u, (F + kGaWarps - 1u) / kGaWarps));
-        for (uint32_t k0 = wid * g; k0 < F; k0 += kGaWarps * g) {
-            const uint32_t j = k0 + lane;
+        for (uint32_t k0 = 0; k0 < F; k0 += kGaWarps * g) {  // strided: warp w takes k0 + w + i * warps (city / country single query -2 %, profiles/r02_ab_cta_strided.jsonl)
+            const uint32_t j = k0 + wid + lane * kGaWarps;
             uint32_t x = 0, p0 = 0, nt = 0;  // x: global vertex id
             if (lane < g && j < F) {
                 const uint32_t li = list[j];

@@ -356,12 +356,15 @@ __global__ void __launch_bounds__(kCtaThreads, (cta_min_blocks<kCtaThreads, A16>
             }
             const uint32_t F = min(s_cnt[p], uint32_t(kListCap));
             // ---- 2. warp-level flattened (vertex, type) pairs; a warp takes g
-            // consecutive list entries so that small frontiers still spread
-            // over all warps
+            // list entries so that small frontiers still spread over all warps
             const uint32_t g = min(32u, max(1u, (F + kCtaWarps - 1u) / kCtaWarps));
             uint32_t imin = kInf;  // minimum improved arrival: feeds the next window base
-            for (uint32_t k0 = wid * g; k0 < F; k0 += kCtaWarps * g) {
-                const uint32_t j = k0 + lane;
+            // warp w takes the list entries k0 + w + i * warps (strided: the
+            // selected vertices of one bitmap word -- spatial neighbours, often
+            // all heavy or all light -- spread over the warps; consecutive
+            // chunks of g entries: -2 %, profiles/r02_ab_cta_strided.jsonl)
+            for (uint32_t k0 = 0; k0 < F; k0 += kCtaWarps * g) {
+                const uint32_t j = k0 + wid + lane * kCtaWarps;
                 uint32_t x = 0, p0 = 0, nt = 0;
                 if (lane < g && j < F) {
                     x = s_list[j];
@@ -593,10 +596,13 @@ __device__ __forceinline__ void grid_solve(const DevIndex &ix, const GridWork &w
             const uint64_t wid = gtid >> 5, nwarps = gsz >> 5;
             uint64_t gg = (cnt + nwarps - 1) / nwarps;
             const uint32_t g = uint32_t(gg < 1 ? 1 : (gg > 32 ? 32 : gg));
-            for (uint64_t k0 = wid * g; k0 < cnt; k0 += nwarps * g) {
+            // strided: warp w takes entries k0 + w + i * warps (metro batch +1.4 %,
+            // profiles/r02_ab_cta_strided.jsonl)
+            for (uint64_t k0 = 0; k0 < cnt; k0 += nwarps * g) {
+                const uint64_t qi = k0 + wid + uint64_t(lane) * nwarps;
                 uint32_t x = 0, p0 = 0, nt = 0;
-                if (lane < g && k0 + lane < cnt) {
-                    x = ld_cg(qc + k0 + lane);
+                if (lane < g && qi < cnt) {
+                    x = ld_cg(qc + qi);
                     const uint32_t ex = ld_cg(w.arr + x);
                     if (ex <= thr) {
                         p0 = __ldg(ix.type_ptr + x);
