@@ -13,6 +13,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
+from paper_1912_00966_b200 import _lib  # noqa: E402
+
+if os.environ.get("EAT_AB_LIB"):  # A/B of a libeat build (tools/build_variant.py)
+    _lib.LIB_PATH = os.path.abspath(os.environ["EAT_AB_LIB"])
 from paper_1912_00966_b200 import Engine, pinned_empty  # noqa: E402
 
 tt = synth.generate("city")
